@@ -1,0 +1,45 @@
+"""The plan rule of DESIGN.md section 5, restated independently of the CUDA library.
+
+Tests hand these plans to the oracle (so no oracle input comes from the CUDA path)
+and check that the library's ``gbs_plan`` reports the same numbers.
+
+A plan is a list of levels [(L, s), ...]; level k+1 sorts the buckets of level k
+(its problem capacity is level k's tight bucket bound).  An empty plan means a
+single on-chip sort.
+"""
+
+TILE_KEYS = 1 << 15     # u32 keys per CTA tile (128 KB of shared memory)
+TILE_PAIRS = 1 << 14    # (key, value) pairs per CTA tile
+D_MIN = 8               # a single level needs d = L/s >= 8 (samples <= n/8)
+D_NEST = 32             # d of a level whose buckets need a nested level
+
+
+def hi_bound(cap: int, L: int, s: int) -> int:
+    """Tight upper bucket bound n'/s + (m-1)(d-1), n' = ceil(cap/L) L."""
+    m = -(-cap // L)
+    d = L // s
+    return m * L // s + (m - 1) * (d - 1)
+
+
+def plan(n: int, tile: int = TILE_KEYS, cfg=None):
+    levels = []
+    cap = n
+    if cfg is not None and n > 1:          # explicit level-1 (L, s), e.g. the paper's
+        levels.append(tuple(cfg))          # (2048, 64) of P:249-250
+        cap = hi_bound(n, *cfg)
+    while cap > tile:
+        L = tile
+        chosen = None
+        s = 2
+        while s <= L // D_MIN:
+            if hi_bound(cap, L, s) <= tile:
+                chosen = s
+                break
+            s *= 2
+        if chosen is not None:
+            levels.append((L, chosen))
+            break
+        s = L // D_NEST
+        levels.append((L, s))
+        cap = hi_bound(cap, L, s)
+    return levels

@@ -1,0 +1,354 @@
+#!/usr/bin/env python
+"""Benchmark: GPU Bucket Sort (arXiv 1002.4464) on B200 -- sorted keys/s, device-timed.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload C2|C3|C1]
+                    [--dist uniform] [--impl gbs|reference]
+
+One step = one complete sort (all nine steps of Alg. 1) of one batch of
+synthetic keys already resident in HBM.  N = 1: the workload BASELINE.json's metric is
+quoted on (configs[1], C2: n = 2^25 uniform u32 keys).  N > 1 (torchrun, one rank per
+GPU, NCCL): every rank holds an n-key shard and the ranks run the multi-GPU sort
+(sample allgather + bucket exchange) -- weak scaling, value = all keys
+sorted / max-over-ranks device time.
+
+Between timed steps the input is restored from a pristine copy and L2 is flushed
+(a 256 MiB device memset), both outside the per-step CUDA-event window.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    "C1": (1 << 16, "C1: n=2^16 uniform u32 keys"),
+    "C2": (1 << 25, "C2: n=2^25 (32M) uniform u32 keys (configs[1]; the paper's largest GTX 285 size)"),
+    "C3": (1 << 26, "C3: n=2^26 (64M) u32 keys"),
+}
+METRIC = "sorted keys/sec (device-timed)"
+L2_FLUSH_BYTES = 256 << 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="C2", choices=sorted(WORKLOADS))
+    ap.add_argument("--dist", default="uniform")
+    ap.add_argument("--impl", default="gbs", choices=["gbs", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- clocks (NVML)
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons with NVML while the timed region runs."""
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # noqa: BLE001
+            self.nv = None
+            self.err = str(e)
+        self.t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        nv = self.nv
+        names = {getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8): "hw_slowdown",
+                 getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40): "hw_thermal_slowdown",
+                 getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20): "sw_thermal_slowdown",
+                 getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4): "sw_power_cap"}
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in names.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.nv:
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.nv:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": self.err}
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------- helpers
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, b.copy_(a) read+write)"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def traffic_from_profile(step_kernel: str):
+    """dram bytes per launch of the dominant kernel from the committed ncu --set full summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_full_summary.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d["kernels"][step_kernel]["dram_bytes_per_launch"]
+    except Exception:  # noqa: BLE001
+        return None
+
+
+def algorithmic_bytes(n: int, plan: dict):
+    """Bytes each level-1 step must move, u32 keys."""
+    L, s = plan["levels"][0]
+    m = plan["m"][0]
+    ms = m * s
+    return {
+        2: 8 * n + 8 * ms,          # Steps 2-3: read + write every key, write the samples
+        4: None,                    # Step 4: recursive sample sort (reported as time only)
+        5: 16 * s,                  # Step 5: gather s splitters
+        6: 4 * n + 8 * s * m + 4 * ms,  # Step 6: key reload, splitters per CTA, counts
+        7: 12 * ms,                 # Step 7: read a twice, write l
+        8: 8 * n + 8 * ms,          # Step 8: read + write every key, a and l rows
+        9: 8 * n + 4 * s,           # Step 9: read + write every key
+    }
+
+
+STEP_NAMES = {2: "k_local_sort (Steps 2-3)", 4: "Step 4 (recursive sample sort)", 5: "k_global_samples (Step 5)",
+              6: "k_sample_index (Step 6)", 7: "k_scan (Step 7)", 8: "k_relocate (Step 8)",
+              9: "k_segment_sort (Step 9)"}
+
+
+# ----------------------------------------------------------------- reference arm (the oracle)
+
+def run_reference(args):
+    import numpy as np
+    import gbs_inputs as gi
+    import oracle
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from plans import plan as plan_rule
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    n_full, wl = WORKLOADS[args.workload]
+    n = min(n_full, 1 << 22)                        # bounded sample: ~1.5 s of CPU per step
+    keys = gi.generate(args.dist, n, seed=0)
+    pl = plan_rule(n)
+    for _ in range(args.warmup):
+        oracle.gbs_sort(keys, plan=pl)
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        out, _, _ = oracle.gbs_sort(keys, plan=pl)
+        ts.append(time.perf_counter() - t0)
+    ms = 1e3 * statistics.mean(ts)
+    v = n / (ms / 1e3)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "keys/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": wl, "n": n_full, "dist": args.dist},
+            "cpu_baseline": {"value": v, "unit": "keys/s", "cores": 1, "kind": "oracle",
+                             "sample": f"{n} keys of the {args.workload} workload per step "
+                                       f"(oracle plan {pl}), single-threaded C"},
+            "e2e": {"value": v, "unit": "keys/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+# ----------------------------------------------------------------- GPU arm
+
+def cpu_baseline_line(args, n):
+    """The oracle as it stands, single-threaded, on the full workload once (~15 s)."""
+    import numpy as np
+    import gbs_inputs as gi
+    import oracle
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from plans import plan as plan_rule
+    keys = gi.generate(args.dist, n, seed=0)
+    t0 = time.perf_counter()
+    oracle.gbs_sort(keys, plan=plan_rule(n))
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": "keys/s", "cores": 1, "kind": "oracle",
+            "sample": f"one full {args.workload} sort ({n} keys, {args.dist}) by the single-threaded C "
+                      f"oracle, {dt:.1f} s"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    import gbs_inputs as gi
+    import paper_1002_4464_b200 as gbs
+    from paper_1002_4464_b200 import _build
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    if rank == 0:
+        _build.build()
+    if world > 1:
+        dist.barrier()
+
+    n, wl = WORKLOADS[args.workload]
+    stream = torch.cuda.current_stream()
+    # rank r holds global elements [r n, (r+1) n) of an N = world*n array
+    pristine = gi.generate_torch(args.dist, n * world if args.dist == "sorted" else n * (rank + 1), seed=0,
+                                 device=dev, start=0 if args.dist == "sorted" else n * rank,
+                                 count=None if args.dist != "sorted" else None)
+    if args.dist == "sorted":
+        pristine = pristine[n * rank:n * (rank + 1)].clone()
+    keys = torch.empty_like(pristine)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+    ws = gbs.Workspace(dev)
+    comm = gbs.Comm() if world > 1 else None
+    out = None
+    if comm is not None:
+        _, cap = gbs.dist_workspace_size(n, world)
+        out = torch.empty(cap, dtype=torch.int32, device=dev)
+    plan = gbs.plan(n)
+
+    def one_sort():
+        if comm is None:
+            gbs.sort_keys(keys, ws=ws)
+        else:
+            gbs.sort_keys_dist(keys, comm, out=out, ws=ws)
+
+    for _ in range(args.warmup):
+        keys.copy_(pristine)
+        one_sort()
+    torch.cuda.synchronize()
+    # correctness of the timed configuration (single GPU): compare with the plain definition
+    if comm is None:
+        ref = torch.sort(pristine.to(torch.int64) & 0xFFFFFFFF).values
+        assert torch.equal(keys.to(torch.int64) & 0xFFFFFFFF, ref), "sort mismatch"
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    if comm is None:
+        gbs.profile_begin()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            keys.copy_(pristine)
+            flush.zero_()                                   # L2 flush (256 MiB > 126 MB L2)
+            starts[i].record(stream)
+            one_sort()
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+    prof = gbs.profile_end() if comm is None else None
+    if world > 1:
+        dist.barrier()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    ms = statistics.mean(step_ms)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    total_keys = n * world
+    value = total_keys / (ms / 1e3)
+
+    # ---- end to end through the C-ABI with host buffers (N = 1)
+    e2e = None
+    if comm is None:
+        host = pristine.cpu().pin_memory()
+        hbuf = torch.empty_like(host).pin_memory()
+        dbuf = torch.empty_like(keys)
+        for _ in range(2):
+            hbuf.copy_(host)
+            gbs.sort_keys_host(hbuf, dbuf, ws=ws)
+        torch.cuda.synchronize()
+        e_ms = []
+        for i in range(max(3, args.steps // 2)):
+            hbuf.copy_(host)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            gbs.sort_keys_host(hbuf, dbuf, ws=ws)
+            b.record(stream)
+            b.synchronize()
+            e_ms.append(a.elapsed_time(b))
+        em = statistics.mean(e_ms)
+        e2e = {"value": n / (em / 1e3), "unit": "keys/s", "h2d_bytes_per_step": 4 * n,
+               "d2h_bytes_per_step": 4 * n, "ms_per_step": em}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peak, peak_src = peaks()
+    roof = None
+    steps = None
+    if prof is not None and prof["calls"]:
+        calls = prof["calls"]
+        ab = algorithmic_bytes(n, plan)
+        steps = {}
+        for k in (2, 4, 5, 6, 7, 8, 9):
+            t_ms = prof[k] / calls
+            gbps = (ab[k] / (t_ms / 1e3) / 1e9) if ab[k] and t_ms > 0 else None
+            steps[STEP_NAMES[k]] = {"ms": round(t_ms, 4), "share": round(prof[k] / sum(prof[j] for j in (2, 4, 5, 6, 7, 8, 9)), 3),
+                                    "alg_bytes": ab[k], "alg_GBps": round(gbps, 1) if gbps else None}
+        dom = max((2, 9, 8, 6), key=lambda k: prof[k])
+        t_ms = prof[dom] / calls
+        ach = ab[dom] / (t_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "kernel": STEP_NAMES[dom], "achieved": round(ach, 1), "peak": peak,
+                "unit": "GB/s", "frac": round(ach / peak, 4), "peak_source": peak_src,
+                "traffic": traffic_from_profile(STEP_NAMES[dom].split()[0]),
+                "alg_bytes_per_launch": ab[dom], "launch_ms": round(t_ms, 4)}
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_line(args, n)
+
+    line = {"metric": METRIC, "value": value, "unit": "keys/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": wl, "n_per_gpu": n, "dist": args.dist,
+                       "plan": plan["levels"], "bucket_bound": plan["bucket_bound"],
+                       "l2": "flushed between steps (256 MiB memset) outside the event window",
+                       "parallelism": f"dp{world}" if world > 1 else "single"},
+            "e2e": e2e, "gpu_launches": plan["kernels_per_sort"] * args.steps,
+            "clocks": clk.summary(), "roofline": roof, "cpu_baseline": cpu, "steps_breakdown": steps,
+            "step_ms_min_max": [min(step_ms), max(step_ms)]}
+    print(json.dumps(line))
+    if world > 1:
+        comm.close()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,172 @@
+/*
+ * gbs.h -- C-ABI of libgbs.so: GPU Bucket Sort, the deterministic sample sort of
+ * Dehne & Zaboli, "Deterministic Sample Sort For GPUs" (arXiv 1002.4464),
+ * Algorithm 1, as hand-written sm_100a kernels.
+ *
+ * Problem statement: "Input: an array A with n data items stored in
+ * global memory.  Output: Array A sorted."  Items are 32-bit unsigned keys in
+ * ascending unsigned order (the paper never fixes the item width; R1),
+ * optionally with 32-bit values that move with their keys (stable by key, R7).
+ *
+ * Conventions (all entry points):
+ *   - Device pointers are caller-owned CUDA global memory on the current device;
+ *     the library allocates no device memory (except NCCL internals in
+ *     gbs_comm_init).  Workspace is caller-provided, sized by the *_workspace_size
+ *     queries, 256-byte aligned.
+ *   - Every argument is validated BEFORE anything is enqueued; on a
+ *     validation error nothing is enqueued.  n = 0 and n = 1 succeed with no work.
+ *   - Work is enqueued on `stream` and completes asynchronously; device faults
+ *     surface as GBS_ERROR_CUDA from this or a later call.  No call aborts or
+ *     throws; gbs_last_error() holds a thread-local message for the last failure.
+ *   - The result is bit-identical across runs and streams (deterministic: no
+ *     atomics decide any output position).
+ *   - Calls on distinct buffers/workspaces/streams may run concurrently.
+ *   - Limits: n <= 2^31 items per call (32-bit tags, R10).
+ */
+#ifndef GBS_H_
+#define GBS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* gbs_stream_t; /* == cudaStream_t; NULL = legacy default stream */
+
+typedef enum {
+    GBS_SUCCESS = 0,
+    GBS_ERROR_INVALID_VALUE = 1,       /* NULL with n > 1, bad config, keys/vals overlap */
+    GBS_ERROR_WORKSPACE_TOO_SMALL = 2, /* ws_bytes < the *_workspace_size query */
+    GBS_ERROR_UNSUPPORTED = 3,         /* n > 2^31, device is not sm_100 */
+    GBS_ERROR_CUDA = 4,                /* launch/runtime error (see gbs_last_error) */
+    GBS_ERROR_NCCL = 5                 /* NCCL error in a multi-GPU call */
+} gbs_status_t;
+
+/* ------------------------------------------------------------ single GPU */
+
+/* Bytes of device workspace gbs_sort_keys needs for n keys (depends on n only). */
+gbs_status_t gbs_sort_keys_workspace_size(size_t n, size_t* bytes);
+
+/* Sort d_keys[0..n) ascending (unsigned), IN PLACE (Alg. 1).
+ * d_keys: device, 4-byte aligned.  d_ws: device workspace of >= the queried size. */
+gbs_status_t gbs_sort_keys(uint32_t* d_keys, size_t n, void* d_ws, size_t ws_bytes,
+                           gbs_stream_t stream);
+
+gbs_status_t gbs_sort_pairs_workspace_size(size_t n, size_t* bytes);
+
+/* Sort (d_keys[i], d_vals[i]) pairs by key, IN PLACE, stable: equal keys keep their
+ * input order (equals std::stable_sort by key; R7).  Keys and values must not overlap. */
+gbs_status_t gbs_sort_pairs(uint32_t* d_keys, uint32_t* d_vals, size_t n, void* d_ws,
+                            size_t ws_bytes, gbs_stream_t stream);
+
+/* End to end from HOST buffers: copy h_keys (pinned host, n keys) to d_keys, sort,
+ * copy back to h_keys; all three enqueued on `stream` (H2D + sort + D2H). */
+gbs_status_t gbs_sort_keys_host(uint32_t* h_keys, size_t n, uint32_t* d_keys, void* d_ws,
+                                size_t ws_bytes, gbs_stream_t stream);
+
+/* ------------------------------------------------------------ plans, stages */
+
+/* Optional explicit level-1 parameters: sublist size L (= n/m of Step 1)
+ * and sample count s (Steps 3/5).  L, s powers of two, 1 <= s <= L,
+ * L <= tile capacity (32768 keys, 16384 pairs).  {0, 0} = automatic plan. */
+typedef struct {
+    uint32_t L;
+    uint32_t s;
+} gbs_config_t;
+
+#define GBS_MAX_LEVELS 4
+/* The static plan (depends on n, item kind and config only -- never on the data).
+ * Level k+1, if present, sorts the buckets of level k (its problem capacity is
+ * level k's tight bucket bound, cap[k+1] = bucket_bound[k]). */
+typedef struct {
+    int levels;                            /* 0 = a single on-chip sort */
+    uint32_t L[GBS_MAX_LEVELS];
+    uint32_t s[GBS_MAX_LEVELS];
+    uint32_t m[GBS_MAX_LEVELS];            /* sublists per problem */
+    uint64_t cap[GBS_MAX_LEVELS];          /* problem capacity at this level */
+    uint64_t bucket_bound[GBS_MAX_LEVELS]; /* n'/s + (m-1)(d-1) */
+    size_t ws_bytes;
+    int kernels_per_sort;                  /* launches one call enqueues */
+} gbs_plan_t;
+
+/* pairs = 0: keys only; 1: key-value pairs.  cfg may be NULL. */
+gbs_status_t gbs_plan(size_t n, int pairs, const gbs_config_t* cfg, gbs_plan_t* out);
+
+gbs_status_t gbs_workspace_size_ex(size_t n, int pairs, const gbs_config_t* cfg, size_t* bytes);
+
+/* Where the level-1 intermediates live inside the workspace (byte offsets), for
+ * stage parity (tests).  Matrices are row-major [i*s + j] with m rows, s columns.
+ *   samples:   m*s uint64 (key << 32 | tag); sorted in place by Step 4
+ *   splitters: s uint64 (Step 5 global samples)
+ *   a, l:      m*s uint32 (Step 6 bucket sizes, Step 7 offsets)
+ *   relocated: n uint32 keys (Step 8 array R = B_1..B_s); pairs: values follow at
+ *              relocated_vals.  Offsets are (size_t)-1 for a single-level-0 plan. */
+typedef struct {
+    size_t samples, splitters, a, l, relocated, relocated_vals;
+} gbs_layout_t;
+gbs_status_t gbs_debug_layout(size_t n, int pairs, const gbs_config_t* cfg, gbs_layout_t* out);
+
+/* Like gbs_sort_keys / gbs_sort_pairs (d_vals may be NULL) with an explicit config,
+ * stopping after level-1 Step `stop_after_step` (2..8; 0 = run to completion). */
+gbs_status_t gbs_sort_ex(uint32_t* d_keys, uint32_t* d_vals, size_t n, const gbs_config_t* cfg,
+                         int stop_after_step, void* d_ws, size_t ws_bytes, gbs_stream_t stream);
+
+/* Per-step device time of level 1 (CUDA events recorded on the call's stream between
+ * the steps' launches) for every complete sort this thread enqueues between begin and
+ * end.  ms[2] = Steps 2-3 (local sort + local sampling), ms[4] = Step 4 (sample sort),
+ * ms[5..8] = Steps 5-8, ms[9] = Step 9 (bucket sort or nested level); summed over
+ * `calls` sorts.  gbs_profile_end synchronises the recorded events. */
+typedef struct {
+    float ms[10];
+    int calls;
+} gbs_step_times_t;
+gbs_status_t gbs_profile_begin(void);
+gbs_status_t gbs_profile_end(gbs_step_times_t* out);
+
+const char* gbs_status_string(gbs_status_t s);
+const char* gbs_last_error(void); /* thread-local */
+
+/* ------------------------------------------------------------ multi GPU */
+/* One process per GPU; a collective over all ranks of `comm` (DESIGN.md 7,
+ * SURVEY 8(e)): every rank sorts its shard with the single-GPU path (E1), takes
+ * s_r regular samples (E2), allgathers them (E3, NCCL), sorts them and picks p
+ * splitters identically on every rank (E4-E5), cuts its sorted shard (E6),
+ * allgathers the p x p counts (E7), exchanges buckets with grouped send/recv over
+ * NVLink (E8) and sorts what it received (E9). */
+typedef struct gbs_comm* gbs_comm_t;
+#define GBS_UNIQUE_ID_BYTES 128 /* == sizeof(ncclUniqueId) */
+
+gbs_status_t gbs_get_unique_id(uint8_t id[GBS_UNIQUE_ID_BYTES]);
+/* Uses the current CUDA device.  Collective: every rank calls it with the same id. */
+gbs_status_t gbs_comm_init(gbs_comm_t* comm, const uint8_t id[GBS_UNIQUE_ID_BYTES], int nranks,
+                           int rank);
+gbs_status_t gbs_comm_destroy(gbs_comm_t comm);
+
+/* out_capacity = n_local + (p-1)(n_local/s_r - 1): the tight receive bound. */
+gbs_status_t gbs_sort_keys_dist_workspace_size(size_t n_local, int nranks, size_t* ws_bytes,
+                                               size_t* out_capacity);
+
+/* Every rank passes the same n_local (>= 2 * s_r).  d_keys (n_local keys) is sorted
+ * in place locally (E1) and then read by the exchange; d_out receives this rank's
+ * part of the global order, *n_out (host) its length.  Concatenating d_out[0:n_out]
+ * in rank order gives sorted(concatenation of the inputs in rank order).  The call
+ * synchronises `stream` once (NCCL needs host-side counts, E7). */
+gbs_status_t gbs_sort_keys_dist(gbs_comm_t comm, uint32_t* d_keys, size_t n_local,
+                                uint32_t* d_out, size_t out_capacity, size_t* n_out, void* d_ws,
+                                size_t ws_bytes, gbs_stream_t stream);
+
+/* Host-only exchange plan (E7-E8), exported so the protocol can be tested without a
+ * GPU.  cuts: p x p row-major, cuts[r*p + k] = cut_{r,k} (#items of rank r's sorted
+ * shard <= splitter k; cuts[r*p + p-1] = n_local).  For `rank`, fills send_off/
+ * send_cnt (into its shard) and recv_off/recv_cnt (into d_out, rank order) for each
+ * peer, and *n_out.  Returns GBS_ERROR_INVALID_VALUE on inconsistent cuts. */
+gbs_status_t gbs_exchange_plan(const uint64_t* cuts, int p, int rank, uint64_t* send_off,
+                               uint64_t* send_cnt, uint64_t* recv_off, uint64_t* recv_cnt,
+                               uint64_t* n_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GBS_H_ */

@@ -1,0 +1,306 @@
+"""GPU Bucket Sort for B200 -- Python binding of libgbs.so (include/gbs.h).
+
+Argument marshalling only: every step of the sort runs in the sm_100a kernels of
+``libgbs.so`` (csrc/).  PyTorch supplies device memory, streams and process
+groups.  There is no CPU fallback: if the library is missing or no sm_100 device
+is present, every call raises.
+
+    import paper_1002_4464_b200 as gbs
+    gbs.sort_keys(t)              # t: CUDA int32/uint32 tensor, sorted in place (unsigned)
+    gbs.sort_pairs(k, v)          # stable by key, in place
+    out = gbs.sort_keys_dist(t)   # one process per GPU (torch.distributed initialised)
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+__all__ = ["lib", "GbsError", "plan", "workspace_size", "debug_layout", "sort_keys", "sort_pairs",
+           "sort_ex", "sort_keys_host", "Workspace", "get_unique_id", "Comm", "sort_keys_dist",
+           "exchange_plan", "dist_workspace_size"]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgbs.so")
+MAX_LEVELS = 4
+UNIQUE_ID_BYTES = 128
+
+
+class GbsError(RuntimeError):
+    pass
+
+
+class Config(C.Structure):
+    _fields_ = [("L", C.c_uint32), ("s", C.c_uint32)]
+
+
+class PlanT(C.Structure):
+    _fields_ = [("levels", C.c_int), ("L", C.c_uint32 * MAX_LEVELS), ("s", C.c_uint32 * MAX_LEVELS),
+                ("m", C.c_uint32 * MAX_LEVELS), ("cap", C.c_uint64 * MAX_LEVELS),
+                ("bucket_bound", C.c_uint64 * MAX_LEVELS), ("ws_bytes", C.c_size_t),
+                ("kernels_per_sort", C.c_int)]
+
+
+class StepTimes(C.Structure):
+    _fields_ = [("ms", C.c_float * 10), ("calls", C.c_int)]
+
+
+class LayoutT(C.Structure):
+    _fields_ = [(f, C.c_size_t) for f in ("samples", "splitters", "a", "l", "relocated", "relocated_vals")]
+
+
+_lib = None
+
+
+def lib():
+    """Load libgbs.so (built in-tree by __graft_entry__.build()); raise if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise GbsError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        p, sz, u32 = C.c_void_p, C.c_size_t, C.c_uint32
+        sigs = {
+            "gbs_sort_keys_workspace_size": [sz, C.POINTER(sz)],
+            "gbs_sort_pairs_workspace_size": [sz, C.POINTER(sz)],
+            "gbs_sort_keys": [p, sz, p, sz, p],
+            "gbs_sort_pairs": [p, p, sz, p, sz, p],
+            "gbs_sort_keys_host": [p, sz, p, p, sz, p],
+            "gbs_plan": [sz, C.c_int, C.POINTER(Config), C.POINTER(PlanT)],
+            "gbs_workspace_size_ex": [sz, C.c_int, C.POINTER(Config), C.POINTER(sz)],
+            "gbs_debug_layout": [sz, C.c_int, C.POINTER(Config), C.POINTER(LayoutT)],
+            "gbs_sort_ex": [p, p, sz, C.POINTER(Config), C.c_int, p, sz, p],
+            "gbs_get_unique_id": [p],
+            "gbs_comm_init": [C.POINTER(p), p, C.c_int, C.c_int],
+            "gbs_comm_destroy": [p],
+            "gbs_sort_keys_dist_workspace_size": [sz, C.c_int, C.POINTER(sz), C.POINTER(sz)],
+            "gbs_sort_keys_dist": [p, p, sz, p, sz, C.POINTER(sz), p, sz, p],
+            "gbs_exchange_plan": [p, C.c_int, C.c_int, p, p, p, p, p],
+            "gbs_profile_begin": [],
+            "gbs_profile_end": [C.POINTER(StepTimes)],
+        }
+        for name, args in sigs.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = C.c_int
+        L.gbs_status_string.argtypes = [C.c_int]
+        L.gbs_status_string.restype = C.c_char_p
+        L.gbs_last_error.argtypes = []
+        L.gbs_last_error.restype = C.c_char_p
+        _lib = L
+    return _lib
+
+
+def _check(rc):
+    if rc != 0:
+        L = lib()
+        raise GbsError(f"{L.gbs_status_string(rc).decode()} ({rc}): {L.gbs_last_error().decode()}")
+
+
+def _cfg(cfg):
+    if cfg is None:
+        return None
+    L, s = cfg
+    return C.byref(Config(L, s))
+
+
+# ----------------------------------------------------------------- plans
+
+def plan(n: int, pairs: bool = False, cfg=None) -> dict:
+    """The static plan for n items (depends on n, kind and cfg only)."""
+    out = PlanT()
+    _check(lib().gbs_plan(n, int(pairs), _cfg(cfg), C.byref(out)))
+    k = out.levels
+    return dict(levels=[(out.L[i], out.s[i]) for i in range(k)], m=list(out.m[:k]), cap=list(out.cap[:k]),
+                bucket_bound=list(out.bucket_bound[:k]), ws_bytes=out.ws_bytes,
+                kernels_per_sort=out.kernels_per_sort)
+
+
+def workspace_size(n: int, pairs: bool = False, cfg=None) -> int:
+    b = C.c_size_t()
+    _check(lib().gbs_workspace_size_ex(n, int(pairs), _cfg(cfg), C.byref(b)))
+    return b.value
+
+
+def debug_layout(n: int, pairs: bool = False, cfg=None) -> dict:
+    out = LayoutT()
+    _check(lib().gbs_debug_layout(n, int(pairs), _cfg(cfg), C.byref(out)))
+    return {f: getattr(out, f) for f, _ in LayoutT._fields_}
+
+
+def profile_begin():
+    _check(lib().gbs_profile_begin())
+
+
+def profile_end() -> dict:
+    """{step: total ms} over the sorts enqueued since profile_begin(), and 'calls'."""
+    out = StepTimes()
+    _check(lib().gbs_profile_end(C.byref(out)))
+    d = {k: out.ms[k] for k in (2, 4, 5, 6, 7, 8, 9)}
+    d["calls"] = out.calls
+    return d
+
+
+# ----------------------------------------------------------------- tensors
+
+def _torch():
+    import torch
+    return torch
+
+
+def _dev_ptr(t, name):
+    torch = _torch()
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise GbsError(f"{name} must be a CUDA tensor")
+    if t.dtype not in (torch.int32, torch.uint32):
+        raise GbsError(f"{name} must be int32/uint32 (bits read as unsigned)")
+    if not t.is_contiguous():
+        raise GbsError(f"{name} must be contiguous")
+    return t.data_ptr()
+
+
+def _stream(stream):
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+class Workspace:
+    """A reusable device workspace (uint8 tensor) grown on demand."""
+
+    def __init__(self, device=None):
+        self.device = device
+        self.buf = None
+
+    def get(self, nbytes: int):
+        torch = _torch()
+        if self.buf is None or self.buf.numel() < nbytes:
+            self.buf = torch.empty(max(nbytes, 256), dtype=torch.uint8,
+                                   device=self.device or torch.cuda.current_device())
+        return self.buf
+
+
+def _ws_for(nbytes, ws, device):
+    if ws is None:
+        ws = Workspace(device)
+    buf = ws.get(nbytes)
+    return C.c_void_p(buf.data_ptr()), buf.numel()
+
+
+def sort_keys(keys, ws: Workspace | None = None, stream=None):
+    """Sort a CUDA int32/uint32 tensor in place, ascending as unsigned 32-bit."""
+    n = keys.numel()
+    kp = _dev_ptr(keys, "keys")
+    need = workspace_size(n)
+    wp, wb = _ws_for(need, ws, keys.device)
+    _check(lib().gbs_sort_keys(C.c_void_p(kp), n, wp, wb, _stream(stream)))
+    return keys
+
+
+def sort_pairs(keys, vals, ws: Workspace | None = None, stream=None):
+    """Sort (key, value) pairs by key in place, stable (std::stable_sort by key)."""
+    n = keys.numel()
+    if vals.numel() != n:
+        raise GbsError("keys and vals must have the same length")
+    kp, vp = _dev_ptr(keys, "keys"), _dev_ptr(vals, "vals")
+    need = workspace_size(n, pairs=True)
+    wp, wb = _ws_for(need, ws, keys.device)
+    _check(lib().gbs_sort_pairs(C.c_void_p(kp), C.c_void_p(vp), n, wp, wb, _stream(stream)))
+    return keys, vals
+
+
+def sort_ex(keys, vals=None, cfg=None, stop_after_step: int = 0, ws=None, stream=None):
+    """Debug/experiment entry: explicit level-1 (L, s) and early stop after a step.
+    ``ws`` may be a raw uint8 CUDA tensor (to read intermediates at debug_layout offsets)."""
+    torch = _torch()
+    n = keys.numel()
+    kp = _dev_ptr(keys, "keys")
+    vp = _dev_ptr(vals, "vals") if vals is not None else None
+    need = workspace_size(n, vals is not None, cfg)
+    if isinstance(ws, torch.Tensor):
+        if ws.numel() < need:
+            raise GbsError("workspace tensor too small")
+        wp, wb = C.c_void_p(ws.data_ptr()), ws.numel()
+    else:
+        wp, wb = _ws_for(need, ws, keys.device)
+    _check(lib().gbs_sort_ex(C.c_void_p(kp), C.c_void_p(vp) if vp else None, n, _cfg(cfg),
+                             stop_after_step, wp, wb, _stream(stream)))
+    return keys
+
+
+def sort_keys_host(h_keys, d_buf, ws: Workspace | None = None, stream=None):
+    """End-to-end: pinned host int32/uint32 tensor -> device -> sort -> host (in place)."""
+    torch = _torch()
+    if h_keys.is_cuda or not h_keys.is_pinned():
+        raise GbsError("h_keys must be a pinned host tensor")
+    n = h_keys.numel()
+    dp = _dev_ptr(d_buf, "d_buf")
+    if d_buf.numel() < n:
+        raise GbsError("d_buf too small")
+    need = workspace_size(n)
+    wp, wb = _ws_for(need, ws, d_buf.device)
+    _check(lib().gbs_sort_keys_host(C.c_void_p(h_keys.data_ptr()), n, C.c_void_p(dp), wp, wb,
+                                    _stream(stream)))
+    return h_keys
+
+
+# ----------------------------------------------------------------- multi GPU
+
+def get_unique_id() -> bytes:
+    buf = (C.c_uint8 * UNIQUE_ID_BYTES)()
+    _check(lib().gbs_get_unique_id(buf))
+    return bytes(buf)
+
+
+def dist_workspace_size(n_local: int, nranks: int):
+    w, cap = C.c_size_t(), C.c_size_t()
+    _check(lib().gbs_sort_keys_dist_workspace_size(n_local, nranks, C.byref(w), C.byref(cap)))
+    return w.value, cap.value
+
+
+def exchange_plan(cuts, rank: int):
+    """Host-only exchange plan (E7-E8) from the p x p cut matrix (numpy uint64)."""
+    import numpy as np
+    cuts = np.ascontiguousarray(cuts, dtype=np.uint64)
+    p = cuts.shape[0]
+    so, sc, ro, rc = (np.zeros(p, np.uint64) for _ in range(4))
+    n_out = np.zeros(1, np.uint64)
+    ptr = lambda a: a.ctypes.data_as(C.c_void_p)
+    _check(lib().gbs_exchange_plan(ptr(cuts), p, rank, ptr(so), ptr(sc), ptr(ro), ptr(rc), ptr(n_out)))
+    return dict(send_off=so, send_cnt=sc, recv_off=ro, recv_cnt=rc, n_out=int(n_out[0]))
+
+
+class Comm:
+    """NCCL communicator of libgbs, bootstrapped over a torch.distributed group."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.rank = dist.get_rank(group)
+        self.nranks = dist.get_world_size(group)
+        obj = [get_unique_id() if self.rank == 0 else None]
+        dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0,
+                                   group=group)
+        idbuf = (C.c_uint8 * UNIQUE_ID_BYTES).from_buffer_copy(obj[0])
+        h = C.c_void_p()
+        _check(lib().gbs_comm_init(C.byref(h), idbuf, self.nranks, self.rank))
+        self.handle = h
+
+    def close(self):
+        if self.handle:
+            _check(lib().gbs_comm_destroy(self.handle))
+            self.handle = None
+
+
+def sort_keys_dist(keys, comm: Comm, out=None, ws: Workspace | None = None, stream=None):
+    """Every rank passes an equal-length shard; ``keys`` is sorted locally in place and
+    the rank's part of the global order is returned (a view of ``out``)."""
+    torch = _torch()
+    n = keys.numel()
+    kp = _dev_ptr(keys, "keys")
+    need, cap = dist_workspace_size(n, comm.nranks)
+    if out is None or out.numel() < cap:
+        out = torch.empty(cap, dtype=keys.dtype, device=keys.device)
+    wp, wb = _ws_for(need, ws, keys.device)
+    n_out = C.c_size_t()
+    _check(lib().gbs_sort_keys_dist(comm.handle, C.c_void_p(kp), n, C.c_void_p(out.data_ptr()), out.numel(),
+                                    C.byref(n_out), wp, wb, _stream(stream)))
+    return out[:n_out.value]

@@ -1,0 +1,591 @@
+// gbs_api.cu -- planner, launch sequence and C-ABI of libgbs.so (include/gbs.h).
+//
+// The plan is static: it depends on (n, item kind, config) only, never on the data
+// (the paper's guaranteed bucket sizes, make every grid size known up
+// front), so a sort is a fixed, host-sync-free sequence of launches on one stream
+// (CUDA-graph capturable).  See DESIGN.md section 5 for the plan rule.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <type_traits>
+#include <vector>
+
+#include "../../include/gbs.h"
+#include "gbs_internal.h"
+#include "gbs_kernels.cuh"
+
+namespace gbs {
+
+// ----------------------------------------------------------------- errors
+static thread_local char g_err[512] = "";
+
+static gbs_status_t fail(gbs_status_t st, const char* fmt, ...)
+{
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof g_err, fmt, ap);
+    va_end(ap);
+    return st;
+}
+
+#define GBS_CUDA(call)                                                                     \
+    do {                                                                                   \
+        cudaError_t e_ = (call);                                                           \
+        if (e_ != cudaSuccess)                                                             \
+            return fail(GBS_ERROR_CUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_),   \
+                        __FILE__, __LINE__);                                               \
+    } while (0)
+
+#define GBS_LAUNCHED()                                                                     \
+    do {                                                                                   \
+        cudaError_t e_ = cudaGetLastError();                                               \
+        if (e_ != cudaSuccess)                                                             \
+            return fail(GBS_ERROR_CUDA, "kernel launch: %s (%s:%d)", cudaGetErrorString(e_), \
+                        __FILE__, __LINE__);                                               \
+    } while (0)
+
+// ----------------------------------------------------------------- step profiling
+// Per-step CUDA events on the call's stream for the top level (gbs_profile_begin/end).
+static thread_local bool g_prof = false;
+static thread_local std::vector<std::array<cudaEvent_t, 8>> g_prof_calls;
+
+struct ProfMarks {
+    cudaEvent_t* ev = nullptr;
+    cudaStream_t st = nullptr;
+    int next = 0;
+    void mark()
+    {
+        if (ev) cudaEventRecord(ev[next++], st);
+    }
+};
+
+// ----------------------------------------------------------------- plan
+constexpr uint32_t TILE_KEYS = 1u << 15;   // u32 keys per CTA tile
+constexpr uint32_t TILE_PAIRS = 1u << 14;  // pairs per CTA tile (u64 on chip + values)
+constexpr uint32_t TILE_U64 = 1u << 14;    // u64 composites per CTA tile
+constexpr uint32_t SMALL_TILE = 2048;      // small CTA configuration
+constexpr uint32_t D_MIN = 8;              // single level needs d >= 8
+constexpr uint32_t D_NEST = 32;            // d of a level with a nested Step 9
+constexpr uint32_t MAX_S = 4096;           // shared-memory limit of Steps 6 and 8
+constexpr int IDX_BLOCK = 512;             // Steps 6 and 8 CTA size
+
+static uint32_t tile_of(int kind) { return kind == KIND_KEYS ? TILE_KEYS : (kind == KIND_PAIRS ? TILE_PAIRS : TILE_U64); }
+static size_t key_bytes(int kind) { return kind == KIND_U64 ? 8 : 4; }
+
+static uint64_t hi_bound(uint64_t cap, uint32_t L, uint32_t s)
+{
+    const uint64_t m = (cap + L - 1) / L, d = L / s;
+    return m * L / s + (m - 1) * (d - 1);
+}
+
+struct Node {
+    int kind = 0;
+    uint32_t B = 1;
+    uint64_t N = 0;
+    bool leaf = false, small = false;
+    uint32_t L = 0, s = 0, m = 0, d = 0;
+    uint64_t Np = 0, hi = 0;
+    uint32_t pad_base = 0;
+    bool local_small = false, bucket_small = false;
+    int step4 = -1, step9 = -1;
+    size_t o_samples = 0, o_splitters = 0, o_a = 0, o_l = 0, o_state = 0;
+    size_t o_child_off = 0, o_child_len = 0, o_reloc = SIZE_MAX, o_reloc_v = SIZE_MAX;
+};
+
+struct Plan {
+    std::vector<Node> nodes;
+    size_t ws = 0;
+    int launches = 0;
+    size_t alloc(size_t bytes)
+    {
+        const size_t o = ws;
+        ws += (bytes + 255) / 256 * 256;
+        return o;
+    }
+};
+
+static bool pow2(uint64_t x) { return x && !(x & (x - 1)); }
+
+// Returns node index, or -1 with g_err set.
+static int build_node(Plan& P, int kind, uint32_t B, uint64_t N, uint32_t pad_base, const gbs_config_t* cfg,
+                      bool own_reloc)
+{
+    const uint32_t tile = tile_of(kind);
+    Node nd;
+    nd.kind = kind;
+    nd.B = B;
+    nd.N = N;
+    nd.pad_base = pad_base;
+    const bool use_cfg = cfg && cfg->L;
+    if (!use_cfg && N <= tile) {
+        nd.leaf = true;
+        nd.small = N <= SMALL_TILE;
+        P.launches += 1;
+        P.nodes.push_back(nd);
+        return (int)P.nodes.size() - 1;
+    }
+    uint32_t L, s = 0;
+    if (use_cfg) {
+        L = cfg->L;
+        s = cfg->s;
+    } else {
+        L = tile;
+        for (uint32_t c = 2; c <= L / D_MIN; c *= 2)
+            if (hi_bound(N, L, c) <= tile) { s = c; break; }
+        if (!s) s = L / D_NEST;
+    }
+    nd.L = L;
+    nd.s = s;
+    nd.m = (uint32_t)((N + L - 1) / L);
+    nd.d = L / s;
+    nd.Np = (uint64_t)nd.m * L;
+    nd.hi = hi_bound(N, L, s);
+    if (nd.Np >= (1ull << 32) - (1ull << 20)) { snprintf(g_err, sizeof g_err, "problem too large for 32-bit tags"); return -1; }
+    if (kind == KIND_U64 && (uint64_t)pad_base + nd.Np >= (1ull << 32)) { snprintf(g_err, sizeof g_err, "sentinel tag overflow"); return -1; }
+    nd.local_small = L <= SMALL_TILE;
+    const uint64_t ms = (uint64_t)B * nd.m * s;
+    nd.o_samples = P.alloc(ms * 8);
+    nd.o_splitters = P.alloc((uint64_t)B * s * 8);
+    nd.o_a = P.alloc(ms * 4);
+    nd.o_l = P.alloc(ms * 4);
+    nd.o_state = P.alloc((uint64_t)B * ((s + 31) / 32) * 8);
+    if (own_reloc) {
+        nd.o_reloc = P.alloc((uint64_t)B * N * key_bytes(kind));
+        if (kind == KIND_PAIRS) nd.o_reloc_v = P.alloc((uint64_t)B * N * 4);
+    }
+    P.launches += 5;  // local sort, global samples, sample index, scan, relocate
+    const int idx = (int)P.nodes.size();
+    P.nodes.push_back(nd);
+    const uint32_t child_pad = kind == KIND_U64 ? pad_base + (uint32_t)(nd.Np - N) : (uint32_t)nd.Np;
+    const int c4 = build_node(P, KIND_U64, B, (uint64_t)nd.m * s, child_pad, nullptr, true);
+    if (c4 < 0) return -1;
+    P.nodes[idx].step4 = c4;
+    if (nd.hi <= tile) {
+        P.nodes[idx].bucket_small = nd.hi <= SMALL_TILE;
+        P.launches += 1;
+    } else {
+        P.nodes[idx].o_child_off = P.alloc((uint64_t)B * s * 8);
+        P.nodes[idx].o_child_len = P.alloc((uint64_t)B * s * 4);
+        P.launches += 1;
+        const uint64_t nb = (uint64_t)B * s;
+        if (nb >= (1ull << 31)) { snprintf(g_err, sizeof g_err, "too many nested problems"); return -1; }
+        const int c9 = build_node(P, kind, (uint32_t)nb, nd.hi, child_pad, nullptr, false);
+        if (c9 < 0) return -1;
+        P.nodes[idx].step9 = c9;
+    }
+    return idx;
+}
+
+static gbs_status_t make_plan(size_t n, int kind, const gbs_config_t* cfg, Plan& P)
+{
+    if (n > (1ull << 31)) return fail(GBS_ERROR_UNSUPPORTED, "n = %zu > 2^31", n);
+    if (cfg && (cfg->L || cfg->s)) {
+        const uint32_t L = cfg->L, s = cfg->s;
+        if (!pow2(L) || !pow2(s) || s > L || L > tile_of(kind) || s > MAX_S)
+            return fail(GBS_ERROR_INVALID_VALUE, "bad config L=%u s=%u (powers of two, s<=L<=%u, s<=%u)", L, s,
+                        tile_of(kind), MAX_S);
+    }
+    P = Plan();
+    if (n <= 1) return GBS_SUCCESS;
+    const gbs_config_t* c = (cfg && cfg->L) ? cfg : nullptr;
+    if (build_node(P, kind, 1, n, 0, c, true) < 0) return fail(GBS_ERROR_UNSUPPORTED, "%s", g_err);
+    return GBS_SUCCESS;
+}
+
+// ----------------------------------------------------------------- launches
+template <typename K>
+static void set_smem(K kernel, size_t bytes)
+{
+    if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+template <int KIND, int BLOCK, int ITEMS>
+static void launch_local_t(const LevelDev& lv, cudaStream_t st)
+{
+    const size_t sm = Seg<KIND, BLOCK, ITEMS>::smem_bytes();
+    static std::once_flag f;
+    std::call_once(f, [&] { set_smem(k_local_sort<KIND, BLOCK, ITEMS>, sm); });
+    k_local_sort<KIND, BLOCK, ITEMS><<<lv.B * lv.m, BLOCK, sm, st>>>(lv);
+}
+
+template <int KIND, int BLOCK, int ITEMS, int MODE>
+static void launch_seg_t(const LevelDev& lv, unsigned grid, cudaStream_t st)
+{
+    const size_t sm = Seg<KIND, BLOCK, ITEMS>::smem_bytes();
+    static std::once_flag f;
+    std::call_once(f, [&] { set_smem(k_segment_sort<KIND, BLOCK, ITEMS, MODE>, sm); });
+    k_segment_sort<KIND, BLOCK, ITEMS, MODE><<<grid, BLOCK, sm, st>>>(lv);
+}
+
+// big / small CTA configurations per kind
+#define GBS_BIG_KEYS 512, 64
+#define GBS_BIG_WIDE 512, 32
+#define GBS_SMALL 256, 8
+
+template <int KIND>
+static void launch_local(const LevelDev& lv, bool small, cudaStream_t st)
+{
+    if (small) launch_local_t<KIND, GBS_SMALL>(lv, st);
+    else if constexpr (KIND == KIND_KEYS) launch_local_t<KIND, GBS_BIG_KEYS>(lv, st);
+    else launch_local_t<KIND, GBS_BIG_WIDE>(lv, st);
+}
+
+template <int KIND, int MODE>
+static void launch_seg(const LevelDev& lv, bool small, unsigned grid, cudaStream_t st)
+{
+    if (small) launch_seg_t<KIND, GBS_SMALL, MODE>(lv, grid, st);
+    else if constexpr (KIND == KIND_KEYS) launch_seg_t<KIND, GBS_BIG_KEYS, MODE>(lv, grid, st);
+    else launch_seg_t<KIND, GBS_BIG_WIDE, MODE>(lv, grid, st);
+}
+
+template <int KIND>
+static void launch_index(const LevelDev& lv, cudaStream_t st)
+{
+    const size_t sm = (size_t)lv.s * 8 + (size_t)(lv.s + (lv.s & 1)) * 4 + (size_t)lv.L * key_bytes(KIND);
+    static std::once_flag f;
+    std::call_once(f, [&] { set_smem(k_sample_index<KIND, IDX_BLOCK>, 227 * 1024); });
+    k_sample_index<KIND, IDX_BLOCK><<<lv.B * lv.m, IDX_BLOCK, sm, st>>>(lv);
+}
+
+template <int KIND>
+static void launch_relocate(const LevelDev& lv, cudaStream_t st)
+{
+    const size_t sm = ((size_t)2 * lv.s + lv.L) * 4;
+    static std::once_flag f;
+    std::call_once(f, [&] { set_smem(k_relocate<KIND, IDX_BLOCK>, 220 * 1024); });
+    k_relocate<KIND, IDX_BLOCK><<<lv.B * lv.m, IDX_BLOCK, sm, st>>>(lv);
+}
+
+struct Bufs {
+    void *in, *reloc, *out;
+    uint32_t *in_v, *reloc_v, *out_v;
+};
+
+template <int KIND>
+static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, Probs pr, cudaStream_t st, int stop);
+
+static gbs_status_t exec(const Plan& P, int ni, char* ws, const Bufs& bf, Probs pr, cudaStream_t st, int stop)
+{
+    switch (P.nodes[ni].kind) {
+        case KIND_KEYS: return exec_kind<KIND_KEYS>(P, ni, ws, bf, pr, st, stop);
+        case KIND_PAIRS: return exec_kind<KIND_PAIRS>(P, ni, ws, bf, pr, st, stop);
+        default: return exec_kind<KIND_U64>(P, ni, ws, bf, pr, st, stop);
+    }
+}
+
+template <int KIND>
+static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, Probs pr, cudaStream_t st, int stop)
+{
+    const Node& nd = P.nodes[ni];
+    LevelDev lv;
+    memset(&lv, 0, sizeof lv);
+    lv.pr = pr;
+    lv.B = nd.B;
+    lv.N = (uint32_t)nd.N;
+    lv.pad_base = nd.pad_base;
+    lv.in = bf.in;
+    lv.reloc = bf.reloc;
+    lv.out = bf.out;
+    lv.in_v = bf.in_v;
+    lv.reloc_v = bf.reloc_v;
+    lv.out_v = bf.out_v;
+    if (nd.leaf) {
+        launch_seg<KIND, MODE_LEAF>(lv, nd.small, nd.B, st);
+        GBS_LAUNCHED();
+        return GBS_SUCCESS;
+    }
+    lv.L = nd.L;
+    lv.s = nd.s;
+    lv.d = nd.d;
+    lv.m = nd.m;
+    lv.samples = reinterpret_cast<u64*>(ws + nd.o_samples);
+    lv.splitters = reinterpret_cast<u64*>(ws + nd.o_splitters);
+    lv.a = reinterpret_cast<uint32_t*>(ws + nd.o_a);
+    lv.l = reinterpret_cast<uint32_t*>(ws + nd.o_l);
+    lv.state = reinterpret_cast<unsigned long long*>(ws + nd.o_state);
+    ProfMarks pm;
+    if (g_prof && ni == 0 && stop == 0) {
+        std::array<cudaEvent_t, 8> evs;
+        for (auto& e : evs) cudaEventCreate(&e);
+        g_prof_calls.push_back(evs);
+        pm.ev = g_prof_calls.back().data();
+        pm.st = st;
+    }
+    pm.mark();
+
+    // Steps 2-3: local sort + local samples (one CTA per sublist)
+    launch_local<KIND>(lv, nd.local_small, st);
+    GBS_LAUNCHED();
+    if (stop == 2 || stop == 3) return GBS_SUCCESS;
+    pm.mark();
+
+    // Step 4: sort the B*m*s samples = a U64 level on B problems of m*s composites
+    {
+        const Node& c = P.nodes[nd.step4];
+        Bufs b4{lv.samples, c.leaf ? (void*)lv.samples : (void*)(ws + c.o_reloc), lv.samples, nullptr, nullptr, nullptr};
+        Probs p4{nullptr, nullptr, (uint64_t)nd.m * nd.s, nd.m * nd.s};
+        gbs_status_t r = exec(P, nd.step4, ws, b4, p4, st, 0);
+        if (r) return r;
+    }
+    if (stop == 4) return GBS_SUCCESS;
+    pm.mark();
+
+    // Step 5: global samples
+    {
+        const uint64_t tot = (uint64_t)nd.B * nd.s;
+        k_global_samples<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(lv);
+        GBS_LAUNCHED();
+    }
+    if (stop == 5) return GBS_SUCCESS;
+    pm.mark();
+
+    // Step 6: sample indexing -> a
+    launch_index<KIND>(lv, st);
+    GBS_LAUNCHED();
+    if (stop == 6) return GBS_SUCCESS;
+    pm.mark();
+
+    // Step 7: column-major exclusive scan -> l
+    const unsigned nblk = (nd.s + 31) / 32;
+    GBS_CUDA(cudaMemsetAsync(lv.state, 0, (size_t)nd.B * nblk * 8, st));
+    k_scan<<<nd.B * nblk, SCAN_BLOCK, 0, st>>>(lv);
+    GBS_LAUNCHED();
+    if (stop == 7) return GBS_SUCCESS;
+    pm.mark();
+
+    // Step 8: relocation in -> reloc
+    launch_relocate<KIND>(lv, st);
+    GBS_LAUNCHED();
+    if (stop == 8) return GBS_SUCCESS;
+    pm.mark();
+
+    // Step 9: bucket sort reloc -> out (one CTA per bucket) or a nested level
+    if (nd.step9 < 0) {
+        launch_seg<KIND, MODE_BUCKET>(lv, nd.bucket_small, nd.B * nd.s, st);
+        GBS_LAUNCHED();
+    } else {
+        lv.child_off = reinterpret_cast<u64*>(ws + nd.o_child_off);
+        lv.child_len = reinterpret_cast<uint32_t*>(ws + nd.o_child_len);
+        const uint64_t tot = (uint64_t)nd.B * nd.s;
+        k_child_desc<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(lv);
+        GBS_LAUNCHED();
+        Bufs b9{bf.reloc, bf.in, bf.out, bf.reloc_v, bf.in_v, bf.out_v};
+        Probs p9{lv.child_off, lv.child_len, 0, 0};
+        gbs_status_t r = exec(P, nd.step9, ws, b9, p9, st, 0);
+        if (r) return r;
+    }
+    pm.mark();
+    return GBS_SUCCESS;
+}
+
+static gbs_status_t check_device()
+{
+    static int ok = -1;
+    if (ok < 0) {
+        int dev = 0, major = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess) return fail(GBS_ERROR_CUDA, "no CUDA device");
+        if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess)
+            return fail(GBS_ERROR_CUDA, "cannot query device");
+        ok = major == 10 ? 1 : 0;
+    }
+    return ok ? GBS_SUCCESS : fail(GBS_ERROR_UNSUPPORTED, "device is not sm_100 (Blackwell B200)");
+}
+
+static gbs_status_t run_sort(uint32_t* keys, uint32_t* vals, size_t n, const gbs_config_t* cfg, int stop,
+                             void* ws, size_t ws_bytes, cudaStream_t st)
+{
+    const int kind = vals ? KIND_PAIRS : KIND_KEYS;
+    Plan P;
+    gbs_status_t r = make_plan(n, kind, cfg, P);
+    if (r) return r;
+    if (n <= 1) return GBS_SUCCESS;
+    if (!keys) return fail(GBS_ERROR_INVALID_VALUE, "d_keys is NULL");
+    if (((uintptr_t)keys & 3) || (vals && ((uintptr_t)vals & 3)))
+        return fail(GBS_ERROR_INVALID_VALUE, "keys/values must be 4-byte aligned");
+    if (vals) {
+        const uintptr_t k0 = (uintptr_t)keys, k1 = k0 + n * 4, v0 = (uintptr_t)vals, v1 = v0 + n * 4;
+        if (k0 < v1 && v0 < k1) return fail(GBS_ERROR_INVALID_VALUE, "keys and values overlap");
+    }
+    if (ws_bytes < P.ws) return fail(GBS_ERROR_WORKSPACE_TOO_SMALL, "workspace %zu < %zu bytes", ws_bytes, P.ws);
+    if (P.ws && (!ws || ((uintptr_t)ws & 255))) return fail(GBS_ERROR_INVALID_VALUE, "workspace NULL or not 256-byte aligned");
+    if (stop && (stop < 2 || stop > 8)) return fail(GBS_ERROR_INVALID_VALUE, "stop_after_step must be 0 or 2..8");
+    r = check_device();
+    if (r) return r;
+    char* w = reinterpret_cast<char*>(ws);
+    const Node& top = P.nodes[0];
+    Bufs bf{keys, top.leaf ? (void*)keys : (void*)(w + top.o_reloc), keys, vals,
+            (top.leaf || !vals) ? vals : reinterpret_cast<uint32_t*>(w + top.o_reloc_v), vals};
+    Probs pr{nullptr, nullptr, 0, (uint32_t)n};
+    return exec(P, 0, w, bf, pr, st, stop);
+}
+
+gbs_status_t fail_msg(gbs_status_t st, const char* msg) { return fail(st, "%s", msg); }
+
+gbs_status_t sort_u64_ws(size_t n, size_t* bytes)
+{
+    Plan P;
+    gbs_status_t r = make_plan(n, KIND_U64, nullptr, P);
+    if (r) return r;
+    *bytes = P.ws;
+    return GBS_SUCCESS;
+}
+
+gbs_status_t sort_u64_inplace(unsigned long long* d, size_t n, void* ws, size_t ws_bytes, cudaStream_t st)
+{
+    // single-tile only: a multi-level u64 sort would need a sentinel tag base above
+    // every caller tag (R8), which only the recursive Step 4 knows.
+    if (n > TILE_U64) return fail(GBS_ERROR_UNSUPPORTED, "sort_u64_inplace: n > %u", TILE_U64);
+    Plan P;
+    gbs_status_t r = make_plan(n, KIND_U64, nullptr, P);
+    if (r) return r;
+    if (n <= 1) return GBS_SUCCESS;
+    if (ws_bytes < P.ws) return fail(GBS_ERROR_WORKSPACE_TOO_SMALL, "u64 workspace too small");
+    char* w = reinterpret_cast<char*>(ws);
+    const Node& top = P.nodes[0];
+    Bufs bf{d, top.leaf ? (void*)d : (void*)(w + top.o_reloc), d, nullptr, nullptr, nullptr};
+    Probs pr{nullptr, nullptr, 0, (uint32_t)n};
+    return exec(P, 0, w, bf, pr, st, 0);
+}
+
+}  // namespace gbs
+
+using namespace gbs;
+
+extern "C" {
+
+const char* gbs_last_error(void) { return g_err; }
+
+gbs_status_t gbs_profile_begin(void)
+{
+    g_prof = true;
+    return GBS_SUCCESS;
+}
+
+gbs_status_t gbs_profile_end(gbs_step_times_t* out)
+{
+    g_prof = false;
+    if (out) memset(out, 0, sizeof *out);
+    gbs_status_t rc = GBS_SUCCESS;
+    for (auto& evs : g_prof_calls) {
+        if (cudaEventSynchronize(evs[7]) != cudaSuccess) rc = fail(GBS_ERROR_CUDA, "profile event sync failed");
+        static const int step_of[7] = {2, 4, 5, 6, 7, 8, 9};
+        for (int k = 0; k < 7 && out && !rc; ++k) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, evs[k], evs[k + 1]);
+            out->ms[step_of[k]] += ms;
+        }
+        if (out && !rc) out->calls += 1;
+        for (auto e : evs) cudaEventDestroy(e);
+    }
+    g_prof_calls.clear();
+    return rc;
+}
+
+const char* gbs_status_string(gbs_status_t s)
+{
+    switch (s) {
+        case GBS_SUCCESS: return "success";
+        case GBS_ERROR_INVALID_VALUE: return "invalid value";
+        case GBS_ERROR_WORKSPACE_TOO_SMALL: return "workspace too small";
+        case GBS_ERROR_UNSUPPORTED: return "unsupported";
+        case GBS_ERROR_CUDA: return "CUDA error";
+        case GBS_ERROR_NCCL: return "NCCL error";
+    }
+    return "unknown status";
+}
+
+gbs_status_t gbs_workspace_size_ex(size_t n, int pairs, const gbs_config_t* cfg, size_t* bytes)
+{
+    if (!bytes) return fail(GBS_ERROR_INVALID_VALUE, "bytes is NULL");
+    Plan P;
+    gbs_status_t r = make_plan(n, pairs ? KIND_PAIRS : KIND_KEYS, cfg, P);
+    if (r) return r;
+    *bytes = P.ws;
+    return GBS_SUCCESS;
+}
+
+gbs_status_t gbs_sort_keys_workspace_size(size_t n, size_t* bytes) { return gbs_workspace_size_ex(n, 0, nullptr, bytes); }
+gbs_status_t gbs_sort_pairs_workspace_size(size_t n, size_t* bytes) { return gbs_workspace_size_ex(n, 1, nullptr, bytes); }
+
+gbs_status_t gbs_plan(size_t n, int pairs, const gbs_config_t* cfg, gbs_plan_t* out)
+{
+    if (!out) return fail(GBS_ERROR_INVALID_VALUE, "out is NULL");
+    Plan P;
+    gbs_status_t r = make_plan(n, pairs ? KIND_PAIRS : KIND_KEYS, cfg, P);
+    if (r) return r;
+    memset(out, 0, sizeof *out);
+    out->ws_bytes = P.ws;
+    out->kernels_per_sort = P.launches;
+    int ni = P.nodes.empty() ? -1 : 0;
+    while (ni >= 0 && !P.nodes[ni].leaf && out->levels < GBS_MAX_LEVELS) {
+        const Node& nd = P.nodes[ni];
+        const int k = out->levels++;
+        out->L[k] = nd.L;
+        out->s[k] = nd.s;
+        out->m[k] = nd.m;
+        out->cap[k] = nd.N;
+        out->bucket_bound[k] = nd.hi;
+        ni = nd.step9;
+    }
+    return GBS_SUCCESS;
+}
+
+gbs_status_t gbs_debug_layout(size_t n, int pairs, const gbs_config_t* cfg, gbs_layout_t* out)
+{
+    if (!out) return fail(GBS_ERROR_INVALID_VALUE, "out is NULL");
+    Plan P;
+    gbs_status_t r = make_plan(n, pairs ? KIND_PAIRS : KIND_KEYS, cfg, P);
+    if (r) return r;
+    memset(out, 0xff, sizeof *out);
+    if (P.nodes.empty() || P.nodes[0].leaf) return GBS_SUCCESS;
+    const Node& t = P.nodes[0];
+    out->samples = t.o_samples;
+    out->splitters = t.o_splitters;
+    out->a = t.o_a;
+    out->l = t.o_l;
+    out->relocated = t.o_reloc;
+    out->relocated_vals = t.o_reloc_v;
+    return GBS_SUCCESS;
+}
+
+gbs_status_t gbs_sort_keys(uint32_t* d_keys, size_t n, void* d_ws, size_t ws_bytes, gbs_stream_t stream)
+{
+    return run_sort(d_keys, nullptr, n, nullptr, 0, d_ws, ws_bytes, (cudaStream_t)stream);
+}
+
+gbs_status_t gbs_sort_pairs(uint32_t* d_keys, uint32_t* d_vals, size_t n, void* d_ws, size_t ws_bytes,
+                            gbs_stream_t stream)
+{
+    if (n > 1 && !d_vals) return fail(GBS_ERROR_INVALID_VALUE, "d_vals is NULL");
+    return run_sort(d_keys, d_vals, n, nullptr, 0, d_ws, ws_bytes, (cudaStream_t)stream);
+}
+
+gbs_status_t gbs_sort_ex(uint32_t* d_keys, uint32_t* d_vals, size_t n, const gbs_config_t* cfg, int stop_after_step,
+                         void* d_ws, size_t ws_bytes, gbs_stream_t stream)
+{
+    return run_sort(d_keys, d_vals, n, cfg, stop_after_step, d_ws, ws_bytes, (cudaStream_t)stream);
+}
+
+gbs_status_t gbs_sort_keys_host(uint32_t* h_keys, size_t n, uint32_t* d_keys, void* d_ws, size_t ws_bytes,
+                                gbs_stream_t stream)
+{
+    if (n > 1 && (!h_keys || !d_keys)) return fail(GBS_ERROR_INVALID_VALUE, "NULL buffer");
+    if (n == 0) return GBS_SUCCESS;
+    size_t need = 0;
+    gbs_status_t r = gbs_sort_keys_workspace_size(n, &need);
+    if (r) return r;
+    if (ws_bytes < need) return fail(GBS_ERROR_WORKSPACE_TOO_SMALL, "workspace %zu < %zu bytes", ws_bytes, need);
+    cudaStream_t st = (cudaStream_t)stream;
+    GBS_CUDA(cudaMemcpyAsync(d_keys, h_keys, n * 4, cudaMemcpyHostToDevice, st));
+    r = run_sort(d_keys, nullptr, n, nullptr, 0, d_ws, ws_bytes, st);
+    if (r) return r;
+    GBS_CUDA(cudaMemcpyAsync(h_keys, d_keys, n * 4, cudaMemcpyDeviceToHost, st));
+    return GBS_SUCCESS;
+}
+
+}  // extern "C"

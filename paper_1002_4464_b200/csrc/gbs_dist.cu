@@ -1,0 +1,265 @@
+// gbs_dist.cu -- multi-GPU GPU Bucket Sort.
+//
+// The paper is single-GPU.  Across the GPUs of one box we apply Alg. 1 once more as
+// an outer level with one sublist per rank (parallel sorting by regular sampling,
+// the scheme [Schaeffer] behind the paper's bucket bound):
+//   E1 local GBS of the shard (the whole single-GPU path = the outer Step 2)
+//   E2 s_r regular samples per rank, composites (key, global position)  (Step 3)
+//   E3 ncclAllGather of the samples                                       (Step 4 input)
+//   E4 every rank sorts the p*s_r samples identically (no broadcast)      (Step 4)
+//   E5 splitters G_k = sorted[(k+1) s_r - 1]                              (Step 5)
+//   E6 cut points by bisection in the sorted shard                        (Step 6)
+//   E7 allgather of the p x p cut matrix, one D2H + stream sync           (Step 7)
+//   E8 grouped ncclSend/ncclRecv over NVLink: contiguous runs, no pack    (Step 8)
+//   E9 sort of the received runs with the single-GPU path                 (Step 9)
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "gbs_internal.h"
+
+struct gbs_comm {
+    ncclComm_t nc;
+    int nranks, rank;
+    unsigned long long* h_cuts;   // pinned p*p
+};
+
+namespace {
+
+constexpr uint32_t S_R_MAX = 1024;   // regular samples per rank (E2)
+
+// s_r: the largest power of two <= S_R_MAX that divides n_local, so the regular
+// sample positions (k+1) n_l / s_r - 1 are exactly equidistant (d = n_l / s_r).
+uint32_t s_r_of(size_t n_local)
+{
+    uint32_t s = 1;
+    while (s < S_R_MAX && n_local % (2ull * s) == 0) s *= 2;
+    return s;
+}
+
+size_t out_cap(size_t n_local, int p)
+{
+    const size_t d = n_local / s_r_of(n_local);
+    return n_local + (size_t)(p - 1) * (d - 1);
+}
+
+size_t al(size_t x) { return (x + 255) / 256 * 256; }
+
+__global__ void k_dist_samples(const uint32_t* keys, size_t n_local, uint32_t s_r, uint64_t gbase,
+                               unsigned long long* out)
+{
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= s_r) return;
+    const size_t d = n_local / s_r;
+    const size_t pos = (size_t)(k + 1) * d - 1;
+    out[k] = ((unsigned long long)keys[pos] << 32) | (unsigned long long)(uint32_t)(gbase + pos);
+}
+
+// E5 + E6: cut_k = #{pos : (S[pos], gbase + pos) <= G_k}, G_k = sorted[(k+1) s_r - 1].
+__global__ void k_dist_cuts(const uint32_t* keys, size_t n_local, uint64_t gbase, const unsigned long long* sorted,
+                            uint32_t s_r, int p, unsigned long long* cuts)
+{
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= p) return;
+    const unsigned long long g = sorted[(size_t)(k + 1) * s_r - 1];
+    size_t lo = 0, hi = n_local;
+    while (lo < hi) {
+        const size_t mid = (lo + hi) / 2;
+        const unsigned long long c = ((unsigned long long)keys[mid] << 32) | (unsigned long long)(uint32_t)(gbase + mid);
+        if (c <= g) lo = mid + 1; else hi = mid;
+    }
+    cuts[k] = lo;
+}
+
+#define NCCL_OK(call)                                                                     \
+    do {                                                                                  \
+        ncclResult_t r_ = (call);                                                         \
+        if (r_ != ncclSuccess) {                                                          \
+            char b_[256];                                                                 \
+            snprintf(b_, sizeof b_, "%s: %s", #call, ncclGetErrorString(r_));             \
+            return gbs::fail_msg(GBS_ERROR_NCCL, b_);                                     \
+        }                                                                                 \
+    } while (0)
+
+#define CUDA_OK(call)                                                                     \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess) {                                                          \
+            char b_[256];                                                                 \
+            snprintf(b_, sizeof b_, "%s: %s", #call, cudaGetErrorString(e_));             \
+            return gbs::fail_msg(GBS_ERROR_CUDA, b_);                                     \
+        }                                                                                 \
+    } while (0)
+
+struct DistLayout {
+    size_t sort_ws, samples, gathered, cuts, all_cuts, total;
+};
+
+gbs_status_t dist_layout(size_t n_local, int p, DistLayout* L)
+{
+    size_t a = 0, b = 0;
+    gbs_status_t r = gbs_sort_keys_workspace_size(n_local, &a);
+    if (r) return r;
+    r = gbs_sort_keys_workspace_size(out_cap(n_local, p), &b);
+    if (r) return r;
+    const uint32_t s_r = s_r_of(n_local);
+    L->sort_ws = 0;
+    size_t o = al(a > b ? a : b);
+    L->samples = o;  o += al((size_t)s_r * 8);
+    L->gathered = o; o += al((size_t)p * s_r * 8);
+    L->cuts = o;     o += al((size_t)p * 8);
+    L->all_cuts = o; o += al((size_t)p * p * 8);
+    L->total = o;
+    return GBS_SUCCESS;
+}
+
+}  // namespace
+
+extern "C" {
+
+gbs_status_t gbs_exchange_plan(const uint64_t* cuts, int p, int rank, uint64_t* send_off, uint64_t* send_cnt,
+                               uint64_t* recv_off, uint64_t* recv_cnt, uint64_t* n_out)
+{
+    if (!cuts || p < 1 || rank < 0 || rank >= p || !send_off || !send_cnt || !recv_off || !recv_cnt || !n_out)
+        return gbs::fail_msg(GBS_ERROR_INVALID_VALUE, "gbs_exchange_plan: bad arguments");
+    for (int r = 0; r < p; ++r) {
+        for (int k = 1; k < p; ++k)
+            if (cuts[(size_t)r * p + k] < cuts[(size_t)r * p + k - 1])
+                return gbs::fail_msg(GBS_ERROR_INVALID_VALUE, "gbs_exchange_plan: cuts not monotone");
+        if (cuts[(size_t)r * p + p - 1] != cuts[(size_t)rank * p + p - 1])
+            return gbs::fail_msg(GBS_ERROR_INVALID_VALUE, "gbs_exchange_plan: ranks disagree on n_local");
+    }
+    for (int k = 0; k < p; ++k) {
+        const uint64_t lo = k ? cuts[(size_t)rank * p + k - 1] : 0;
+        send_off[k] = lo;
+        send_cnt[k] = cuts[(size_t)rank * p + k] - lo;
+    }
+    uint64_t run = 0;
+    for (int r = 0; r < p; ++r) {
+        const uint64_t lo = rank ? cuts[(size_t)r * p + rank - 1] : 0;
+        recv_cnt[r] = cuts[(size_t)r * p + rank] - lo;
+        recv_off[r] = run;
+        run += recv_cnt[r];
+    }
+    *n_out = run;
+    return GBS_SUCCESS;
+}
+
+gbs_status_t gbs_get_unique_id(uint8_t id[GBS_UNIQUE_ID_BYTES])
+{
+    static_assert(sizeof(ncclUniqueId) == GBS_UNIQUE_ID_BYTES, "ncclUniqueId size");
+    if (!id) return gbs::fail_msg(GBS_ERROR_INVALID_VALUE, "id is NULL");
+    ncclUniqueId u;
+    NCCL_OK(ncclGetUniqueId(&u));
+    memcpy(id, &u, sizeof u);
+    return GBS_SUCCESS;
+}
+
+gbs_status_t gbs_comm_init(gbs_comm_t* comm, const uint8_t id[GBS_UNIQUE_ID_BYTES], int nranks, int rank)
+{
+    if (!comm || !id || nranks < 1 || rank < 0 || rank >= nranks)
+        return gbs::fail_msg(GBS_ERROR_INVALID_VALUE, "gbs_comm_init: bad arguments");
+    ncclUniqueId u;
+    memcpy(&u, id, sizeof u);
+    gbs_comm* c = new (std::nothrow) gbs_comm();
+    if (!c) return gbs::fail_msg(GBS_ERROR_INVALID_VALUE, "out of host memory");
+    c->nranks = nranks;
+    c->rank = rank;
+    if (cudaMallocHost(&c->h_cuts, (size_t)nranks * nranks * 8) != cudaSuccess) {
+        delete c;
+        return gbs::fail_msg(GBS_ERROR_CUDA, "cudaMallocHost failed");
+    }
+    ncclResult_t r = ncclCommInitRank(&c->nc, nranks, u, rank);
+    if (r != ncclSuccess) {
+        cudaFreeHost(c->h_cuts);
+        delete c;
+        return gbs::fail_msg(GBS_ERROR_NCCL, ncclGetErrorString(r));
+    }
+    *comm = c;
+    return GBS_SUCCESS;
+}
+
+gbs_status_t gbs_comm_destroy(gbs_comm_t comm)
+{
+    if (!comm) return GBS_SUCCESS;
+    ncclResult_t r = ncclCommDestroy(comm->nc);
+    cudaFreeHost(comm->h_cuts);
+    delete comm;
+    return r == ncclSuccess ? GBS_SUCCESS : gbs::fail_msg(GBS_ERROR_NCCL, ncclGetErrorString(r));
+}
+
+gbs_status_t gbs_sort_keys_dist_workspace_size(size_t n_local, int nranks, size_t* ws_bytes, size_t* out_capacity)
+{
+    if (!ws_bytes || !out_capacity || nranks < 1) return gbs::fail_msg(GBS_ERROR_INVALID_VALUE, "bad arguments");
+    if ((uint64_t)n_local * nranks > (1ull << 32)) return gbs::fail_msg(GBS_ERROR_UNSUPPORTED, "N > 2^32");
+    if ((size_t)nranks * s_r_of(n_local) > 16384) return gbs::fail_msg(GBS_ERROR_UNSUPPORTED, "too many ranks");
+    DistLayout L;
+    gbs_status_t r = dist_layout(n_local, nranks, &L);
+    if (r) return r;
+    *ws_bytes = L.total;
+    *out_capacity = out_cap(n_local, nranks);
+    return GBS_SUCCESS;
+}
+
+gbs_status_t gbs_sort_keys_dist(gbs_comm_t comm, uint32_t* d_keys, size_t n_local, uint32_t* d_out,
+                                size_t out_capacity, size_t* n_out, void* d_ws, size_t ws_bytes, gbs_stream_t stream)
+{
+    if (!comm || !n_out || (n_local && (!d_keys || !d_out)))
+        return gbs::fail_msg(GBS_ERROR_INVALID_VALUE, "gbs_sort_keys_dist: NULL argument");
+    const int p = comm->nranks, rank = comm->rank;
+    size_t need = 0, cap = 0;
+    gbs_status_t r = gbs_sort_keys_dist_workspace_size(n_local, p, &need, &cap);
+    if (r) return r;
+    if (out_capacity < cap) return gbs::fail_msg(GBS_ERROR_INVALID_VALUE, "out_capacity below the receive bound");
+    if (ws_bytes < need) return gbs::fail_msg(GBS_ERROR_WORKSPACE_TOO_SMALL, "dist workspace too small");
+    if (n_local == 0) { *n_out = 0; return GBS_SUCCESS; }
+    cudaStream_t st = (cudaStream_t)stream;
+    DistLayout L;
+    dist_layout(n_local, p, &L);
+    char* w = reinterpret_cast<char*>(d_ws);
+    const size_t sort_ws = L.samples;
+    const uint32_t s_r = s_r_of(n_local);
+    const uint64_t gbase = (uint64_t)rank * n_local;
+    auto* samples = reinterpret_cast<unsigned long long*>(w + L.samples);
+    auto* gathered = reinterpret_cast<unsigned long long*>(w + L.gathered);
+    auto* cuts = reinterpret_cast<unsigned long long*>(w + L.cuts);
+    auto* all_cuts = reinterpret_cast<unsigned long long*>(w + L.all_cuts);
+
+    r = gbs_sort_keys(d_keys, n_local, w, sort_ws, stream);                            // E1
+    if (r) return r;
+    k_dist_samples<<<(s_r + 255) / 256, 256, 0, st>>>(d_keys, n_local, s_r, gbase, samples);  // E2
+    CUDA_OK(cudaGetLastError());
+    NCCL_OK(ncclAllGather(samples, gathered, s_r, ncclUint64, comm->nc, st));            // E3
+    r = gbs::sort_u64_inplace(gathered, (size_t)p * s_r, nullptr, 0, st);               // E4
+    if (r) return r;
+    k_dist_cuts<<<(p + 127) / 128, 128, 0, st>>>(d_keys, n_local, gbase, gathered, s_r, p, cuts);  // E5-E6
+    CUDA_OK(cudaGetLastError());
+    NCCL_OK(ncclAllGather(cuts, all_cuts, p, ncclUint64, comm->nc, st));                 // E7
+    CUDA_OK(cudaMemcpyAsync(comm->h_cuts, all_cuts, (size_t)p * p * 8, cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaStreamSynchronize(st));
+    std::vector<uint64_t> so(p), sc(p), ro(p), rc(p);
+    uint64_t total = 0;
+    r = gbs_exchange_plan(reinterpret_cast<const uint64_t*>(comm->h_cuts), p, rank, so.data(), sc.data(), ro.data(),
+                          rc.data(), &total);
+    if (r) return r;
+    if (total > out_capacity) return gbs::fail_msg(GBS_ERROR_CUDA, "receive count exceeds the proven bound");
+    NCCL_OK(ncclGroupStart());                                                           // E8
+    for (int k = 0; k < p; ++k) {
+        if (k == rank) continue;
+        if (sc[k]) NCCL_OK(ncclSend(d_keys + so[k], sc[k], ncclUint32, k, comm->nc, st));
+        if (rc[k]) NCCL_OK(ncclRecv(d_out + ro[k], rc[k], ncclUint32, k, comm->nc, st));
+    }
+    NCCL_OK(ncclGroupEnd());
+    if (sc[rank])
+        CUDA_OK(cudaMemcpyAsync(d_out + ro[rank], d_keys + so[rank], sc[rank] * 4, cudaMemcpyDeviceToDevice, st));
+    r = gbs_sort_keys(d_out, total, w, sort_ws, stream);                                 // E9
+    if (r) return r;
+    *n_out = total;
+    return GBS_SUCCESS;
+}
+
+}  // extern "C"

@@ -1,0 +1,189 @@
+"""GPU parity (-m gpu): the CUDA path through the C-ABI vs the CPU oracle, bit-exact.
+
+Integer sort: the final output is unique, every intermediate is fixed
+by the plan and the readings of DESIGN.md section 3, so every comparison is exact
+equality.  Inputs: gbs_inputs (seeded, the seven distributions of the north star)."""
+import numpy as np
+import pytest
+
+import gbs_inputs as gi
+import oracle
+from plans import TILE_KEYS, TILE_PAIRS, plan
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_1002_4464_b200 as gbs  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1002_4464_b200 import _build
+    _build.build()
+    return torch.device("cuda:0")
+
+
+def to_dev(a, dev):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.uint32).view(np.int32)).to(dev)
+
+
+def to_np(t):
+    return t.cpu().numpy().view(np.uint32)
+
+
+def gpu_sort(keys, dev, vals=None, cfg=None, stop=0, ws=None):
+    k = to_dev(keys, dev)
+    v = to_dev(vals, dev) if vals is not None else None
+    gbs.sort_ex(k, v, cfg=cfg, stop_after_step=stop, ws=ws)
+    torch.cuda.synchronize()
+    return to_np(k), (to_np(v) if v is not None else None)
+
+
+SIZES = [0, 1, 2, 3, 31, 1023, 2048, 2049, 32768, 32769, 65536, 100003, 1 << 20, 3 * (1 << 20) + 17]
+
+
+@pytest.mark.parametrize("n", SIZES)
+@pytest.mark.parametrize("dist", gi.DISTRIBUTIONS)
+def test_keys_default_plan(dev, n, dist):
+    keys = gi.generate(dist, n, seed=n % 5)
+    got, _ = gpu_sort(keys, dev)
+    exp, _, _ = oracle.gbs_sort(keys, plan=plan(n, TILE_KEYS))
+    assert np.array_equal(got, exp)
+
+
+@pytest.mark.parametrize("seed", range(5))
+@pytest.mark.parametrize("dist", gi.DISTRIBUTIONS)
+def test_keys_C1_paper_plan(dev, seed, dist):
+    """C1: 2^16 keys with the paper's L = 2K, s = 64."""
+    n = 1 << 16
+    keys = gi.generate(dist, n, seed=seed)
+    got, _ = gpu_sort(keys, dev, cfg=(2048, 64))
+    exp, _, _ = oracle.gbs_sort(keys, plan=plan(n, cfg=(2048, 64)))
+    assert np.array_equal(got, exp)
+
+
+@pytest.mark.parametrize("cfg,n", [((2048, 64), 1 << 16), (None, 1 << 16), (None, 3 * (1 << 20) + 17),
+                                   ((4096, 256), 500_000), ((1024, 32), 300_001)])
+@pytest.mark.parametrize("dist", ["uniform", "zero", "det_duplicates", "staggered"])
+def test_stage_parity(dev, cfg, n, dist):
+    """Every level-1 intermediate equals the oracle's: sorted sublists (Step 2), samples
+    (3), sorted samples (4), splitters (5), a (6), l (7), R (8)."""
+    keys = gi.generate(dist, n, seed=3)
+    pl = plan(n, TILE_KEYS, cfg)
+    _, _, tr = oracle.gbs_sort(keys, plan=pl, trace=True)
+    lay = gbs.debug_layout(n, cfg=cfg)
+    m, s = tr["a"].shape
+    ws = torch.zeros(gbs.workspace_size(n, cfg=cfg), dtype=torch.uint8, device=dev)
+
+    def view(off, count, dtype):
+        nb = count * np.dtype(dtype).itemsize
+        return ws[off:off + nb].cpu().numpy().view(dtype)
+
+    got, _ = gpu_sort(keys, dev, cfg=cfg, stop=2, ws=ws)
+    assert np.array_equal(got, tr["sorted_keys"])
+    assert np.array_equal(view(lay["samples"], m * s, np.uint64), tr["samples"])
+    gpu_sort(keys, dev, cfg=cfg, stop=5, ws=ws)
+    assert np.array_equal(view(lay["samples"], m * s, np.uint64), tr["sorted_samples"])
+    assert np.array_equal(view(lay["splitters"], s, np.uint64), tr["splitters"])
+    gpu_sort(keys, dev, cfg=cfg, stop=8, ws=ws)
+    assert np.array_equal(view(lay["a"], m * s, np.uint32).reshape(m, s), tr["a"])
+    assert np.array_equal(view(lay["l"], m * s, np.uint32).reshape(m, s), tr["l"])
+    assert np.array_equal(view(lay["relocated"], n, np.uint32), tr["relocated"])
+
+
+@pytest.mark.parametrize("n", [2, 1000, 16384, 16385, 65536, 1 << 20, 2_000_003])
+@pytest.mark.parametrize("dist", ["uniform", "zero", "det_duplicates", "sorted", "gaussian"])
+def test_pairs_stable(dev, n, dist):
+    keys = gi.generate(dist, n, seed=1)
+    if dist == "uniform":
+        keys = keys % 1000                         # many duplicates: stability is observable
+    vals = gi.pair_values(n)
+    gk, gv = gpu_sort(keys, dev, vals=vals)
+    ek, ev, _ = oracle.gbs_sort(keys, vals, plan=plan(n, TILE_PAIRS))
+    assert np.array_equal(gk, ek) and np.array_equal(gv, ev)
+
+
+def test_nested_level_keys(dev):
+    """A plan with a nested Step 9 (paper's L = 2K, s = 64 at n = 2^21: bucket bound
+    > one tile) -- the batched level over all buckets."""
+    n = (1 << 21) + 5
+    for dist in ("uniform", "zero", "det_duplicates"):
+        keys = gi.generate(dist, n, seed=2)
+        pl = plan(n, TILE_KEYS, (2048, 64))
+        assert len(pl) == 2
+        got, _ = gpu_sort(keys, dev, cfg=(2048, 64))
+        exp, _, _ = oracle.gbs_sort(keys, plan=pl)
+        assert np.array_equal(got, exp)
+
+
+def test_nested_level_pairs(dev):
+    n = (1 << 20) + 3
+    keys = gi.generate("uniform", n, seed=4) % 5000
+    vals = gi.pair_values(n)
+    pl = plan(n, TILE_PAIRS, (1024, 16))
+    assert len(pl) == 2
+    gk, gv = gpu_sort(keys, dev, vals=vals, cfg=(1024, 16))
+    ek, ev, _ = oracle.gbs_sort(keys, vals, plan=pl)
+    assert np.array_equal(gk, ek) and np.array_equal(gv, ev)
+
+
+def test_determinism_intermediates(dev):
+    n = 1 << 20
+    keys = gi.generate("det_duplicates", n, seed=0)
+    lay = gbs.debug_layout(n)
+    outs = []
+    for _ in range(3):
+        ws = torch.zeros(gbs.workspace_size(n), dtype=torch.uint8, device=dev)
+        got, _ = gpu_sort(keys, dev, stop=8, ws=ws)
+        outs.append(ws[lay["a"]:lay["relocated"]].cpu().numpy().copy())
+    assert all(np.array_equal(outs[0], o) for o in outs[1:])
+
+
+def test_host_e2e_entry(dev):
+    n = 1 << 20
+    keys = gi.generate("uniform", n, seed=7)
+    h = torch.from_numpy(keys.view(np.int32).copy()).pin_memory()
+    d = torch.empty(n, dtype=torch.int32, device=dev)
+    gbs.sort_keys_host(h, d)
+    torch.cuda.synchronize()
+    assert np.array_equal(h.numpy().view(np.uint32), np.sort(keys))
+
+
+@pytest.mark.parametrize("dist", gi.DISTRIBUTIONS)
+def test_C2_C3_full_size(dev, dist):
+    """C2 (2^25 uniform) and C3 (2^26, all seven distributions) in the launch
+    configuration bench.py times; compared with the plain definition (a library sort)."""
+    n = 1 << 26
+    keys = gi.generate_torch(dist, n, seed=0, device=dev)
+    exp = np.sort(keys.cpu().numpy().view(np.uint32))
+    gbs.sort_keys(keys)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_np(keys), exp)
+    if dist == "uniform":
+        k2 = gi.generate_torch(dist, 1 << 25, seed=0, device=dev)
+        exp2, _, _ = oracle.gbs_sort(to_np(k2), plan=plan(1 << 25))
+        gbs.sort_keys(k2)
+        torch.cuda.synchronize()
+        assert np.array_equal(to_np(k2), exp2)
+
+
+def test_dist_single_rank_nccl(dev):
+    """The multi-GPU entry with p = 1 (one NCCL rank): E1-E9 run, output == sort."""
+    import ctypes as C
+    L = gbs.lib()
+    uid = gbs.get_unique_id()
+    h = C.c_void_p()
+    idbuf = (C.c_uint8 * 128).from_buffer_copy(uid)
+    assert L.gbs_comm_init(C.byref(h), idbuf, 1, 0) == 0
+
+    class _C:
+        handle, nranks, rank = h, 1, 0
+    n = 1 << 20
+    keys = gi.generate("staggered", n, seed=1)
+    d = to_dev(keys, dev)
+    out = gbs.sort_keys_dist(d, _C)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_np(out), np.sort(keys))
+    assert L.gbs_comm_destroy(h) == 0

@@ -225,11 +225,10 @@ def main():
     n, wl = WORKLOADS[args.workload]
     stream = torch.cuda.current_stream()
     # rank r holds global elements [r n, (r+1) n) of an N = world*n array
-    pristine = gi.generate_torch(args.dist, n * world if args.dist == "sorted" else n * (rank + 1), seed=0,
-                                 device=dev, start=0 if args.dist == "sorted" else n * rank,
-                                 count=None if args.dist != "sorted" else None)
     if args.dist == "sorted":
-        pristine = pristine[n * rank:n * (rank + 1)].clone()
+        pristine = gi.generate_torch("sorted", n * world, seed=0, device=dev)[n * rank:n * (rank + 1)].clone()
+    else:
+        pristine = gi.generate_torch(args.dist, n * world, seed=0, device=dev, start=n * rank, count=n)
     keys = torch.empty_like(pristine)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
     ws = gbs.Workspace(dev)
@@ -252,6 +251,8 @@ def main():
     torch.cuda.synchronize()
     # correctness of the timed configuration (single GPU): compare with the plain definition
     if comm is None:
+        keys.copy_(pristine)
+        one_sort()
         ref = torch.sort(pristine.to(torch.int64) & 0xFFFFFFFF).values
         assert torch.equal(keys.to(torch.int64) & 0xFFFFFFFF, ref), "sort mismatch"
 

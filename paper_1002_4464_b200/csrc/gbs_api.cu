@@ -74,7 +74,8 @@ constexpr uint32_t D_NEST = 32;            // d of a level with a nested Step 9
 constexpr uint32_t MAX_S = 4096;           // shared-memory limit of Steps 6 and 8
 constexpr int IDX_BLOCK = 512;             // Steps 6 and 8 CTA size
 
-static uint32_t tile_of(int kind) { return kind == KIND_KEYS ? TILE_KEYS : (kind == KIND_PAIRS ? TILE_PAIRS : TILE_U64); }
+static constexpr uint32_t tile_of_c(int kind) { return kind == KIND_KEYS ? TILE_KEYS : (kind == KIND_PAIRS ? TILE_PAIRS : TILE_U64); }
+static uint32_t tile_of(int kind) { return tile_of_c(kind); }
 static size_t key_bytes(int kind) { return kind == KIND_U64 ? 8 : 4; }
 
 static uint64_t hi_bound(uint64_t cap, uint32_t L, uint32_t s)
@@ -255,10 +256,11 @@ static void launch_index(const LevelDev& lv, cudaStream_t st)
 template <int KIND>
 static void launch_relocate(const LevelDev& lv, cudaStream_t st)
 {
-    const size_t sm = ((size_t)2 * lv.s + lv.L) * 4;
+    constexpr int MAXPER = (int)(tile_of_c(KIND) / IDX_BLOCK);
+    const size_t sm = ((size_t)2 * lv.s + lv.L + IDX_BLOCK + 1) * 4;
     static std::once_flag f;
-    std::call_once(f, [&] { set_smem(k_relocate<KIND, IDX_BLOCK>, 220 * 1024); });
-    k_relocate<KIND, IDX_BLOCK><<<lv.B * lv.m, IDX_BLOCK, sm, st>>>(lv);
+    std::call_once(f, [&] { set_smem(k_relocate<KIND, IDX_BLOCK, MAXPER>, 220 * 1024); });
+    k_relocate<KIND, IDX_BLOCK, MAXPER><<<lv.B * lv.m, IDX_BLOCK, sm, st>>>(lv);
 }
 
 struct Bufs {

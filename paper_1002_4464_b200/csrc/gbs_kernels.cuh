@@ -347,14 +347,16 @@ __device__ __forceinline__ int upper_bound_u32(const uint32_t* a, int lo, int hi
     return lo;
 }
 
-template <int KIND, int BLOCK>
-__global__ void __launch_bounds__(BLOCK) k_relocate(LevelDev lv)
+// MAXPER = max items per thread (L / BLOCK): the sublist is prefetched into registers
+// (striped, coalesced) while the destination map is built, then stored.
+template <int KIND, int BLOCK, int MAXPER>
+__global__ void __launch_bounds__(BLOCK, 1) k_relocate(LevelDev lv)
 {
     using KT = typename std::conditional<KIND == KIND_U64, unsigned long long, uint32_t>::type;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint32_t* starts = reinterpret_cast<uint32_t*>(smem_raw);
     uint32_t* delta = starts + lv.s;
-    uint32_t* dest = delta + lv.s;
+    uint32_t* dest = delta + lv.s;          // L + BLOCK entries (one pad slot per `per`)
     __shared__ uint32_t wtmp[32];
 
     const uint32_t b = blockIdx.x / lv.m, i = blockIdx.x % lv.m;
@@ -364,6 +366,16 @@ __global__ void __launch_bounds__(BLOCK) k_relocate(LevelDev lv)
     const int v = len > i0 ? (int)umin64(len - i0, lv.L) : 0;
     if (v == 0) return;
 
+    // prefetch the sublist (striped: r = t + k*BLOCK) -- latency overlaps the map build
+    const KT* src = reinterpret_cast<const KT*>(lv.in) + off + i0;
+    KT x[MAXPER];
+    {
+        const int rem = v - (int)threadIdx.x;
+        const KT* s0 = src + threadIdx.x;
+#pragma unroll
+        for (int k = 0; k < MAXPER; ++k) x[k] = k * BLOCK < rem ? s0[k * BLOCK] : KT(0);
+    }
+
     const uint64_t row = ((uint64_t)b * lv.m + i) * lv.s;
     for (uint32_t j = threadIdx.x; j < lv.s; j += BLOCK) starts[j] = lv.a[row + j];
     __syncthreads();
@@ -371,8 +383,11 @@ __global__ void __launch_bounds__(BLOCK) k_relocate(LevelDev lv)
     for (uint32_t j = threadIdx.x; j < lv.s; j += BLOCK) delta[j] = lv.l[row + j] - starts[j];
     __syncthreads();
 
+    // destination map: thread t walks positions [t*per, t*per + per) (blocked) and
+    // writes dest at r + r/per (padding keeps the blocked writes bank-conflict free)
     const int S = (int)lv.s;
-    const int per = (v + BLOCK - 1) / BLOCK;
+    const int per = (int)(lv.L / BLOCK) > 0 ? (int)(lv.L / BLOCK) : 1;   // power of two
+    const int lp = 31 - __clz(per);
     const int r0 = threadIdx.x * per, r1 = min(v, r0 + per);
     if (r0 < r1) {
         int j = upper_bound_u32(starts, 0, S, (uint32_t)r0) - 1;
@@ -381,17 +396,29 @@ __global__ void __launch_bounds__(BLOCK) k_relocate(LevelDev lv)
                 ++j;
                 if (j + 1 < S && starts[j + 1] <= (uint32_t)r) j = upper_bound_u32(starts, j + 1, S, (uint32_t)r) - 1;
             }
-            dest[r] = (uint32_t)r + delta[j];
+            dest[r + (r >> lp)] = (uint32_t)r + delta[j];
         }
     }
     __syncthreads();
-    const KT* src = reinterpret_cast<const KT*>(lv.in) + off + i0;
     KT* dst = reinterpret_cast<KT*>(lv.reloc) + off;
-    for (int r = threadIdx.x; r < v; r += BLOCK) dst[dest[r]] = src[r];
+#pragma unroll
+    for (int k = 0; k < MAXPER; ++k) {
+        const int r = threadIdx.x + k * BLOCK;
+        if (r < v) dst[dest[r + (r >> lp)]] = x[k];
+    }
     if (KIND == KIND_PAIRS) {
         const uint32_t* sv = lv.in_v + off + i0;
         uint32_t* dv = lv.reloc_v + off;
-        for (int r = threadIdx.x; r < v; r += BLOCK) dv[dest[r]] = sv[r];
+        uint32_t y[8];
+        for (int r0v = threadIdx.x; r0v < v; r0v += 8 * BLOCK) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) y[u] = r0v + u * BLOCK < v ? sv[r0v + u * BLOCK] : 0u;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int r = r0v + u * BLOCK;
+                if (r < v) dv[dest[r + (r >> lp)]] = y[u];
+            }
+        }
     }
 }
 

@@ -83,15 +83,16 @@ __device__ __forceinline__ void reg_sort(T (&x)[N])
     if constexpr (N > 1) apply_net<T, N>(x, std::make_index_sequence<BatcherNet<N>::C>{});
 }
 
-template <typename T, int BLOCK, int ITEMS>
+template <typename T, int BLOCK, int ITEMS, int CHAINS_ = 0>
 struct CtaSort {
     static constexpr int TILE = BLOCK * ITEMS;
     static constexpr int LOG_ITEMS = Log2<ITEMS>::value;
     static constexpr int WARP_SPAN = 32 * ITEMS;                  // items owned by one warp
     // one pad slot per ITEMS items (bank-conflict-free blocked stores) + 1 overrun slot
     static constexpr int SMEM_ELEMS = TILE + TILE / ITEMS + 1;
-    // independent merge chains per thread (ILP) when registers allow
-    static constexpr int CHAINS = (ITEMS * sizeof(T) <= 128) ? 2 : 1;
+    // independent merge chains per thread (ILP); overridable by the instantiation
+    static constexpr int CHAINS = CHAINS_ > 0 ? CHAINS_ : ((ITEMS * sizeof(T) <= 256) ? 2 : 1);
+    static constexpr T TMAX = ~T(0);
 
     static __device__ __forceinline__ int phys(int p) { return p + (p >> LOG_ITEMS); }
 
@@ -119,61 +120,44 @@ struct CtaSort {
     }
 
     // The thread's ITEMS outputs [start, start+ITEMS) of the merge of the pair of
-    // sorted runs of width w containing `start`, produced as two independent halves
-    // (two merge-path chains interleaved for ILP: each step of a chain waits on one
-    // shared-memory load).
-    static __device__ __forceinline__ void merge_thread1(T (&x)[ITEMS], const T* sm, int start, int w)
-    {
-        const int base = start & ~(2 * w - 1);
-        const int diag = start - base;
-        const int aEnd = base + w, bEnd = base + 2 * w;
-        const int s0 = split(sm, base, w, diag);
-        int ai = base + s0, bi = aEnd + diag - s0;
-        T a = sm[phys(ai)], b = sm[phys(bi)];
-#pragma unroll
-        for (int k = 0; k < ITEMS; ++k) {
-            const bool t = (ai < aEnd) && (bi >= bEnd || a <= b);
-            x[k] = t ? a : b;
-            const int n = (t ? ai : bi) + 1;
-            ai += t ? 1 : 0;
-            bi += t ? 0 : 1;
-            const T v = sm[phys(n)];
-            a = t ? v : a;
-            b = t ? b : v;
-        }
-    }
-
+    // sorted runs (A = [base, base+w), B = [base+w, base+2w)) containing `start`,
+    // produced by CHAINS independent merge-path chains of ITEMS/CHAINS outputs each,
+    // interleaved for ILP (each step of a chain waits on one shared-memory load).
+    // Per chain only the A index is kept: B's index is (2 base + w + diag) - A index.
+    // An exhausted run reads as TMAX ("sticky sentinel"): for keys a tie between a
+    // real 0xFFFFFFFF and the sentinel outputs the same value; u64 items never equal
+    // TMAX.  Ties take A first, so the merge is stable.
     static __device__ __forceinline__ void merge_thread(T (&x)[ITEMS], const T* sm, int start, int w)
     {
-        if constexpr (CHAINS == 1) { merge_thread1(x, sm, start, w); return; }
-        constexpr int H = ITEMS / 2;
+        constexpr int H = ITEMS / CHAINS;
         const int base = start & ~(2 * w - 1);
-        const int diag0 = start - base, diag1 = diag0 + H;
         const int aEnd = base + w, bEnd = base + 2 * w;
-        const int s0 = split(sm, base, w, diag0);
-        const int s1 = split(sm, base, w, diag1);
-        int ai0 = base + s0, bi0 = aEnd + diag0 - s0;
-        int ai1 = base + s1, bi1 = aEnd + diag1 - s1;
-        T a0 = sm[phys(ai0)], b0 = sm[phys(bi0)];
-        T a1 = sm[phys(ai1)], b1 = sm[phys(bi1)];
+        int ai[CHAINS], cb[CHAINS];
+        T a[CHAINS], b[CHAINS];
+#pragma unroll
+        for (int c = 0; c < CHAINS; ++c) {
+            const int diag = start - base + c * H;
+            ai[c] = base + split(sm, base, w, diag);
+            cb[c] = 2 * base + w + diag;              // bi = cb - ai
+            const int bi = cb[c] - ai[c];
+            a[c] = ai[c] < aEnd ? sm[phys(ai[c])] : TMAX;
+            b[c] = bi < bEnd ? sm[phys(bi)] : TMAX;
+        }
 #pragma unroll
         for (int k = 0; k < H; ++k) {
-            const bool t0 = (ai0 < aEnd) && (bi0 >= bEnd || a0 <= b0);
-            const bool t1 = (ai1 < aEnd) && (bi1 >= bEnd || a1 <= b1);
-            x[k] = t0 ? a0 : b0;
-            x[H + k] = t1 ? a1 : b1;
-            const int n0 = (t0 ? ai0 : bi0) + 1;
-            const int n1 = (t1 ? ai1 : bi1) + 1;
-            ai0 += t0 ? 1 : 0;
-            bi0 += t0 ? 0 : 1;
-            ai1 += t1 ? 1 : 0;
-            bi1 += t1 ? 0 : 1;
-            const T v0 = sm[phys(n0)];
-            const T v1 = sm[phys(n1)];
-            a0 = t0 ? v0 : a0;
-            b0 = t0 ? b0 : v0;
-            a1 = t1 ? v1 : a1;
-            b1 = t1 ? b1 : v1;
+#pragma unroll
+            for (int c = 0; c < CHAINS; ++c) {
+                const bool t = a[c] <= b[c];
+                x[c * H + k] = t ? a[c] : b[c];
+                ai[c] += t ? 1 : 0;
+                const int bi = cb[c] + k + 1 - ai[c];
+                const int nidx = t ? ai[c] : bi;
+                const bool ok = nidx < (t ? aEnd : bEnd);
+                T v = sm[phys(nidx)];
+                v = ok ? v : TMAX;
+                a[c] = t ? v : a[c];
+                b[c] = t ? b[c] : v;
+            }
         }
     }
 

@@ -20,7 +20,7 @@ __all__ = ["lib", "GbsError", "plan", "workspace_size", "debug_layout", "sort_ke
            "exchange_plan", "dist_workspace_size"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgbs.so")
+LIB_PATH = os.environ.get("GBS_LIB") or os.path.join(_HERE, "libgbs.so")   # GBS_LIB: tuning builds only
 MAX_LEVELS = 4
 UNIQUE_ID_BYTES = 128
 

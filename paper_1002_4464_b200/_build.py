@@ -30,20 +30,23 @@ def needs_build() -> bool:
     return any(os.path.getmtime(os.path.join(CSRC, d)) > t for d in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+    """Compile libgbs.so in-tree (or to `out` with extra -D `defines`, for tuning runs)."""
+    if out is None and not force and not needs_build():
         return LIB
+    target = out or LIB
     nccl = nccl_root()
     cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
            "-Xcompiler", "-fPIC", "-shared", f"-I{nccl}/include",
            *[os.path.join(CSRC, s) for s in SOURCES],
            f"-L{nccl}/lib", "-l:libnccl.so.2", "-Xlinker", "-rpath", "-Xlinker", f"{nccl}/lib",
-           "-o", LIB + ".tmp"]
+           *[f"-D{d}" for d in defines],
+           "-o", target + ".tmp"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.check_call(cmd)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(target + ".tmp", target)
+    return target
 
 
 if __name__ == "__main__":

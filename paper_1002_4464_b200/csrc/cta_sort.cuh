@@ -83,18 +83,26 @@ __device__ __forceinline__ void reg_sort(T (&x)[N])
     if constexpr (N > 1) apply_net<T, N>(x, std::make_index_sequence<BatcherNet<N>::C>{});
 }
 
-template <typename T, int BLOCK, int ITEMS, int CHAINS_ = 0>
+#ifndef GBS_PAD_SHIFT
+#define GBS_PAD_SHIFT 0   // 0 = one pad slot per ITEMS
+#endif
+
+template <typename T, int BLOCK, int ITEMS, int CHAINS_ = 0, int PAD_ = GBS_PAD_SHIFT>
 struct CtaSort {
     static constexpr int TILE = BLOCK * ITEMS;
     static constexpr int LOG_ITEMS = Log2<ITEMS>::value;
     static constexpr int WARP_SPAN = 32 * ITEMS;                  // items owned by one warp
-    // one pad slot per ITEMS items (bank-conflict-free blocked stores) + 1 overrun slot
-    static constexpr int SMEM_ELEMS = TILE + TILE / ITEMS + 1;
+    // Shared-memory layout: one pad slot every 2^PAD items.  PAD = log2(ITEMS) makes the
+    // blocked stores conflict-free; a finer pad spreads the merge reads, whose lanes sit
+    // ~ITEMS/2 elements apart in each run.
+    static constexpr int PAD = PAD_ > 0 ? PAD_ : LOG_ITEMS;
+    static constexpr int SMEM_ELEMS = TILE + (TILE >> PAD) + 2;
     // independent merge chains per thread (ILP); overridable by the instantiation
     static constexpr int CHAINS = CHAINS_ > 0 ? CHAINS_ : ((ITEMS * sizeof(T) <= 256) ? 2 : 1);
     static constexpr T TMAX = ~T(0);
 
-    static __device__ __forceinline__ int phys(int p) { return p + (p >> LOG_ITEMS); }
+    static __device__ __forceinline__ int phys(int p) { return p + (p >> PAD); }
+    static __device__ __forceinline__ int phys_fma(int p) { return p + (p >> PAD); }
 
     // Position of register slot k of the calling thread in the load order: each warp
     // owns a contiguous span of 32*ITEMS positions, read 32 consecutive at a time
@@ -143,6 +151,27 @@ struct CtaSort {
             a[c] = ai[c] < aEnd ? sm[phys(ai[c])] : TMAX;
             b[c] = bi < bEnd ? sm[phys(bi)] : TMAX;
         }
+        // Fast path (warp-uniform): no lane can exhaust a run inside its H outputs, so
+        // the end-of-run checks (3 ALU-pipe ops per step) are dropped.
+        bool fast = true;
+#pragma unroll
+        for (int c = 0; c < CHAINS; ++c) fast = fast && ai[c] + H <= aEnd && cb[c] - ai[c] + H <= bEnd;
+        if (__all_sync(__activemask(), fast)) {
+#pragma unroll
+            for (int k = 0; k < H; ++k) {
+#pragma unroll
+                for (int c = 0; c < CHAINS; ++c) {
+                    const bool t = a[c] <= b[c];
+                    x[c * H + k] = t ? a[c] : b[c];
+                    ai[c] += t ? 1 : 0;
+                    const int nidx = t ? ai[c] : cb[c] + k + 1 - ai[c];
+                    const T v = sm[phys_fma(nidx)];
+                    a[c] = t ? v : a[c];
+                    b[c] = t ? b[c] : v;
+                }
+            }
+            return;
+        }
 #pragma unroll
         for (int k = 0; k < H; ++k) {
 #pragma unroll
@@ -153,11 +182,49 @@ struct CtaSort {
                 const int bi = cb[c] + k + 1 - ai[c];
                 const int nidx = t ? ai[c] : bi;
                 const bool ok = nidx < (t ? aEnd : bEnd);
-                T v = sm[phys(nidx)];
+                T v = sm[phys_fma(nidx)];
                 v = ok ? v : TMAX;
                 a[c] = t ? v : a[c];
                 b[c] = t ? b[c] : v;
             }
+        }
+    }
+
+    // Tile whose runs of length R (power of two >= ITEMS) are already sorted: load it
+    // into shared memory (phys layout, TMAX beyond valid) and run only the merge levels
+    // w = R, 2R, ... .  Used for Step 4, whose input is m sorted runs of s samples
+    // (each sublist's samples come out of its sorted sublist).  Block-synchronised.
+    template <typename Src>
+    static __device__ __forceinline__ void sort_presorted(Src src, T* sm, int valid, int R)
+    {
+        const int t = threadIdx.x;
+        {
+            T y[ITEMS];
+#pragma unroll
+            for (int k = 0; k < ITEMS; ++k) {
+                const int p = t + k * BLOCK;
+                y[k] = p < valid ? src[p] : TMAX;
+            }
+#pragma unroll
+            for (int k = 0; k < ITEMS; ++k) sm[phys(t + k * BLOCK)] = y[k];
+        }
+        __syncthreads();
+        const int start = t * ITEMS;
+        const int wspan0 = (t >> 5) * WARP_SPAN;
+        T x[ITEMS];
+#pragma unroll 1
+        for (int w = R; w < TILE; w *= 2) {
+            const bool intra = 2 * w <= WARP_SPAN;
+            const bool active = intra ? (wspan0 < valid) : (start < valid);
+            if (active) merge_thread(x, sm, start, w);
+            if (intra) __syncwarp(); else __syncthreads();
+            if (active) {
+#pragma unroll
+                for (int k = 0; k < ITEMS; ++k) sm[phys(start + k)] = x[k];
+            }
+            // the NEXT level's readers decide the barrier: a cross-warp level reads
+            // other warps' stores
+            if (4 * w <= WARP_SPAN) __syncwarp(); else __syncthreads();
         }
     }
 

@@ -224,9 +224,20 @@ static void launch_seg_t(const LevelDev& lv, unsigned grid, cudaStream_t st)
 }
 
 // big / small CTA configurations per kind
-#define GBS_BIG_KEYS 512, 64
-#define GBS_BIG_WIDE 512, 32
+// (overridable with -D for tuning experiments)
+#ifndef GBS_KEYS_BLOCK
+#define GBS_KEYS_BLOCK 1024
+#define GBS_KEYS_ITEMS 32
+#endif
+#ifndef GBS_WIDE_BLOCK
+#define GBS_WIDE_BLOCK 1024
+#define GBS_WIDE_ITEMS 16
+#endif
+#define GBS_BIG_KEYS GBS_KEYS_BLOCK, GBS_KEYS_ITEMS
+#define GBS_BIG_WIDE GBS_WIDE_BLOCK, GBS_WIDE_ITEMS
+#ifndef GBS_SMALL
 #define GBS_SMALL 256, 8
+#endif
 
 template <int KIND>
 static void launch_local(const LevelDev& lv, bool small, cudaStream_t st)
@@ -263,6 +274,17 @@ static void launch_relocate(const LevelDev& lv, cudaStream_t st)
     k_relocate<KIND, IDX_BLOCK, MAXPER><<<lv.B * lv.m, IDX_BLOCK, sm, st>>>(lv);
 }
 
+static uint32_t num_sms()
+{
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    }
+    return (uint32_t)n;
+}
+
 struct Bufs {
     void *in, *reloc, *out;
     uint32_t *in_v, *reloc_v, *out_v;
@@ -296,6 +318,8 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
     lv.in_v = bf.in_v;
     lv.reloc_v = bf.reloc_v;
     lv.out_v = bf.out_v;
+    lv.pf_stride = num_sms();
+    lv.presorted = pr.presorted;
     if (nd.leaf) {
         launch_seg<KIND, MODE_LEAF>(lv, nd.small, nd.B, st);
         GBS_LAUNCHED();
@@ -330,7 +354,8 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
     {
         const Node& c = P.nodes[nd.step4];
         Bufs b4{lv.samples, c.leaf ? (void*)lv.samples : (void*)(ws + c.o_reloc), lv.samples, nullptr, nullptr, nullptr};
-        Probs p4{nullptr, nullptr, (uint64_t)nd.m * nd.s, nd.m * nd.s};
+        // each sublist's s samples are sorted and contiguous: runs of length s
+        Probs p4{nullptr, nullptr, (uint64_t)nd.m * nd.s, nd.m * nd.s, nd.s};
         gbs_status_t r = exec(P, nd.step4, ws, b4, p4, st, 0);
         if (r) return r;
     }

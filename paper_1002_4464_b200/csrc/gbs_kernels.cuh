@@ -31,6 +31,7 @@ struct Probs {
     const uint32_t* len;   // device array or nullptr -> len_c
     uint64_t stride;
     uint32_t len_c;
+    uint32_t presorted;    // inputs are sorted runs of this length (host-side; copied to LevelDev)
     __device__ __forceinline__ uint64_t offset(uint32_t b) const { return off ? off[b] : (uint64_t)b * stride; }
     __device__ __forceinline__ uint32_t length(uint32_t b) const { return len ? len[b] : len_c; }
 };
@@ -53,7 +54,80 @@ struct LevelDev {
     unsigned long long* state;  // [B][ceil(s/32)] decoupled look-back words
     u64* child_off;        // [B*s] nested Step 9 problems
     uint32_t* child_len;
+    uint32_t pf_stride;    // co-resident CTAs (SMs x CTAs/SM): CTA b prefetches CTA b + pf_stride
+    uint32_t presorted;    // input consists of sorted runs of this length (Step 4 levels), 0 = none
 };
+
+// L2 prefetch of a byte range (cp.async.bulk.prefetch: a TMA bulk operation, no
+// registers or shared memory): the CTA of the next wave finds its tile in L2.
+__device__ __forceinline__ void prefetch_l2(const void* p, size_t bytes)
+{
+    if (bytes == 0) return;
+    const uintptr_t a = (uintptr_t)p & ~uintptr_t(15);
+    const uintptr_t e = ((uintptr_t)p + bytes + 15) & ~uintptr_t(15);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((uint32_t)(e - a)) : "memory");
+}
+
+// Copy `bytes` (multiple of 4) from global to shared memory with all threads of the
+// CTA: 16-byte vector loads, 8 in flight per thread, when both sides are 16-byte
+// aligned (warp-uniform check); 4-byte loads otherwise.  Caller synchronises.
+template <int BLOCK>
+__device__ __forceinline__ void stage_to_smem(void* dst, const void* src, size_t bytes)
+{
+    const bool vec = (((uintptr_t)src | (uintptr_t)dst) & 15) == 0;
+    if (vec) {
+        const size_t n16 = bytes / 16;
+        const uint4* s = reinterpret_cast<const uint4*>(src);
+        uint4* d = reinterpret_cast<uint4*>(dst);
+        for (size_t q0 = threadIdx.x; q0 < n16; q0 += 8 * BLOCK) {
+            uint4 r[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (q0 + u * BLOCK < n16) r[u] = __ldg(s + q0 + u * BLOCK);
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (q0 + u * BLOCK < n16) d[q0 + u * BLOCK] = r[u];
+        }
+        for (size_t q = n16 * 4 + threadIdx.x; q < bytes / 4; q += BLOCK)
+            reinterpret_cast<uint32_t*>(dst)[q] = __ldg(reinterpret_cast<const uint32_t*>(src) + q);
+    } else {
+        const size_t n4 = bytes / 4;
+        const uint32_t* s = reinterpret_cast<const uint32_t*>(src);
+        uint32_t* d = reinterpret_cast<uint32_t*>(dst);
+        for (size_t q0 = threadIdx.x; q0 < n4; q0 += 8 * BLOCK) {
+            uint32_t r[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (q0 + u * BLOCK < n4) r[u] = __ldg(s + q0 + u * BLOCK);
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (q0 + u * BLOCK < n4) d[q0 + u * BLOCK] = r[u];
+        }
+    }
+}
+
+// Tile (sublist) of CTA `cta` of a per-sublist kernel: problem offset + i*L, length.
+__device__ __forceinline__ void sublist_of(const LevelDev& lv, uint32_t cta, uint64_t& start, int& v)
+{
+    const uint32_t b = cta / lv.m, i = cta % lv.m;
+    const uint32_t len = lv.pr.length(b);
+    const uint64_t i0 = (uint64_t)i * lv.L;
+    start = lv.pr.offset(b) + i0;
+    v = len > i0 ? (int)(len - i0 < lv.L ? len - i0 : lv.L) : 0;
+}
+
+#ifndef GBS_KEYS_CHAINS
+#define GBS_KEYS_CHAINS 1   // merge chains per thread (0 = automatic); 1 measured best at 1024x32
+#endif
+#ifndef GBS_WIDE_CHAINS
+#define GBS_WIDE_CHAINS 1
+#endif
+#ifndef GBS_PRESORTED
+#define GBS_PRESORTED 1     // Step 4 local sort merges the presorted sample runs only
+#endif
+#ifndef GBS_ADAPT_DEPTH
+#define GBS_ADAPT_DEPTH 2   // Step 9 tile halvings for small buckets
+#endif
 
 template <int KIND> struct ItemT { using T = unsigned long long; };
 template <> struct ItemT<KIND_KEYS> { using T = uint32_t; };
@@ -71,7 +145,8 @@ __device__ __forceinline__ unsigned long long pad64(uint32_t pad_base, uint64_t 
 template <int KIND, int BLOCK, int ITEMS>
 struct Seg {
     using T = typename ItemT<KIND>::T;
-    using CS = CtaSort<T, BLOCK, ITEMS>;
+    using CS = CtaSort<T, BLOCK, ITEMS, (KIND == KIND_KEYS ? GBS_KEYS_CHAINS : GBS_WIDE_CHAINS)>;
+    using KeyT = typename std::conditional<KIND == KIND_U64, unsigned long long, uint32_t>::type;  // in HBM
     static constexpr int TILE = CS::TILE;
     static constexpr size_t smem_bytes()
     {
@@ -146,8 +221,23 @@ __global__ void __launch_bounds__(BLOCK, 1) k_local_sort(LevelDev lv)
     const uint64_t i0 = (uint64_t)i * lv.L;
     const int v = len > i0 ? (int)umin64(len - i0, lv.L) : 0;
 
+    if (threadIdx.x == 0 && blockIdx.x + lv.pf_stride < lv.B * lv.m) {
+        uint64_t ps;
+        int pv;
+        sublist_of(lv, blockIdx.x + lv.pf_stride, ps, pv);
+        prefetch_l2(reinterpret_cast<const char*>(lv.in) + ps * sizeof(typename S::KeyT), (size_t)pv * sizeof(typename S::KeyT));
+        if (KIND == KIND_PAIRS) prefetch_l2(lv.in_v + ps, (size_t)pv * 4);
+    }
     if (v > 0) {
-        S::load_sort(lv.in, lv.in_v, off + i0, v, sm, vsm);
+        bool done = false;
+        if constexpr (KIND == KIND_U64) {
+            if (GBS_PRESORTED && lv.presorted >= (uint32_t)ITEMS) {
+                const unsigned long long* src = reinterpret_cast<const unsigned long long*>(lv.in) + off + i0;
+                S::CS::sort_presorted(src, sm, v, (int)lv.presorted);
+                done = true;
+            }
+        }
+        if (!done) S::load_sort(lv.in, lv.in_v, off + i0, v, sm, vsm);
         S::store(lv.in, lv.in_v, off + i0, v, sm, vsm);
     }
     u64* smp = lv.samples + ((uint64_t)b * lv.m + i) * lv.s;
@@ -200,7 +290,13 @@ __global__ void __launch_bounds__(BLOCK) k_sample_index(LevelDev lv)
     const int v = len > i0 ? (int)umin64(len - i0, lv.L) : 0;
 
     const KT* src = reinterpret_cast<const KT*>(lv.in) + off + i0;
-    for (int p = threadIdx.x; p < v; p += BLOCK) ks[p] = src[p];
+    if (threadIdx.x == 0 && blockIdx.x + lv.pf_stride < lv.B * lv.m) {
+        uint64_t ps;
+        int pv;
+        sublist_of(lv, blockIdx.x + lv.pf_stride, ps, pv);
+        prefetch_l2(reinterpret_cast<const KT*>(lv.in) + ps, (size_t)pv * sizeof(KT));
+    }
+    stage_to_smem<BLOCK>(ks, src, (size_t)v * sizeof(KT));
     const unsigned long long* g = lv.splitters + (uint64_t)b * lv.s;
     for (uint32_t j = threadIdx.x; j < lv.s; j += BLOCK) gs[j] = g[j];
     __syncthreads();
@@ -368,6 +464,13 @@ __global__ void __launch_bounds__(BLOCK, 1) k_relocate(LevelDev lv)
 
     // prefetch the sublist (striped: r = t + k*BLOCK) -- latency overlaps the map build
     const KT* src = reinterpret_cast<const KT*>(lv.in) + off + i0;
+    if (threadIdx.x == 0 && blockIdx.x + lv.pf_stride < lv.B * lv.m) {
+        uint64_t ps;
+        int pv;
+        sublist_of(lv, blockIdx.x + lv.pf_stride, ps, pv);
+        prefetch_l2(reinterpret_cast<const KT*>(lv.in) + ps, (size_t)pv * sizeof(KT));
+        if (KIND == KIND_PAIRS) prefetch_l2(lv.in_v + ps, (size_t)pv * 4);
+    }
     KT x[MAXPER];
     {
         const int rem = v - (int)threadIdx.x;
@@ -428,6 +531,27 @@ __global__ void __launch_bounds__(BLOCK, 1) k_relocate(LevelDev lv)
 // one CTA per whole problem (len_b <= tile).
 enum SegMode { MODE_BUCKET = 0, MODE_LEAF = 1 };
 
+// Sort v items with the smallest tile (ITEMS, ITEMS/2, ITEMS/4 per thread; same CTA)
+// that holds them: every thread stays busy, so a bucket of half the capacity (the
+// average, since the bound is ~2n/s) costs about half.  Block-uniform branch.
+template <int KIND, int BLOCK, int ITEMS, int DEPTH>
+__device__ __forceinline__ void seg_sort_adaptive(const void* src, const uint32_t* src_v, uint64_t off, int v,
+                                                  void* dst, uint32_t* dst_v, unsigned char* smem_raw)
+{
+    if constexpr (DEPTH > 0 && ITEMS >= 8) {
+        if (v <= BLOCK * ITEMS / 2) {
+            seg_sort_adaptive<KIND, BLOCK, ITEMS / 2, DEPTH - 1>(src, src_v, off, v, dst, dst_v, smem_raw);
+            return;
+        }
+    }
+    using S = Seg<KIND, BLOCK, ITEMS>;
+    using T = typename S::T;
+    T* sm = reinterpret_cast<T*>(smem_raw);
+    uint32_t* vsm = reinterpret_cast<uint32_t*>(sm + S::CS::SMEM_ELEMS);
+    S::load_sort(src, src_v, off, v, sm, vsm);
+    S::store(dst, dst_v, off, v, sm, vsm);
+}
+
 template <int KIND, int BLOCK, int ITEMS, int MODE>
 __global__ void __launch_bounds__(BLOCK, 1) k_segment_sort(LevelDev lv)
 {
@@ -458,11 +582,21 @@ __global__ void __launch_bounds__(BLOCK, 1) k_segment_sort(LevelDev lv)
         v = (int)(en - st);
         src = lv.reloc;
         src_v = lv.reloc_v;
+        const uint32_t nxt = blockIdx.x + lv.pf_stride;
+        if (threadIdx.x == 0 && nxt < lv.B * lv.s) {
+            const uint32_t nb = nxt / lv.s, nj = nxt % lv.s;
+            const uint32_t* n0 = lv.l + (uint64_t)nb * lv.m * lv.s;
+            const uint32_t ns = n0[nj], ne = nj + 1 < lv.s ? n0[nj + 1] : lv.pr.length(nb);
+            const uint64_t po = lv.pr.offset(nb) + ns;
+            prefetch_l2(reinterpret_cast<const typename S::KeyT*>(lv.reloc) + po, (size_t)(ne - ns) * sizeof(typename S::KeyT));
+            if (KIND == KIND_PAIRS) prefetch_l2(lv.reloc_v + po, (size_t)(ne - ns) * 4);
+        }
     }
     if (v <= 0) return;
     const uint64_t off = lv.pr.offset(b) + start;
-    S::load_sort(src, src_v, off, v, sm, vsm);
-    S::store(lv.out, lv.out_v, off, v, sm, vsm);
+    (void)sm;
+    (void)vsm;
+    seg_sort_adaptive<KIND, BLOCK, ITEMS, GBS_ADAPT_DEPTH>(src, src_v, off, v, lv.out, lv.out_v, smem_raw);
 }
 
 // Nested Step 9: the buckets of this level become the problems of the next level.

@@ -31,6 +31,7 @@ WORKLOADS = {
     "C1": (1 << 16, "C1: n=2^16 uniform u32 keys"),
     "C2": (1 << 25, "C2: n=2^25 (32M) uniform u32 keys (configs[1]; the paper's largest GTX 285 size)"),
     "C3": (1 << 26, "C3: n=2^26 (64M) u32 keys"),
+    "C4": (1 << 30, "C4: n=2^30 u32->u32 key-value pairs (stable; nested Step 9)"),
 }
 METRIC = "sorted keys/sec (device-timed)"
 L2_FLUSH_BYTES = 256 << 20
@@ -123,19 +124,20 @@ def traffic_from_profile(step_kernel: str):
         return None
 
 
-def algorithmic_bytes(n: int, plan: dict):
-    """Bytes each level-1 step must move, u32 keys."""
+def algorithmic_bytes(n: int, plan: dict, ib: int = 4):
+    """Bytes each level-1 step must move; ib = 4 keys, 8 pairs."""
     L, s = plan["levels"][0]
     m = plan["m"][0]
     ms = m * s
+    nested = len(plan["levels"]) > 1
     return {
-        2: 8 * n + 8 * ms,          # Steps 2-3: read + write every key, write the samples
+        2: 2 * ib * n + 8 * ms,     # Steps 2-3: read + write every item, write the samples
         4: None,                    # Step 4: recursive sample sort (reported as time only)
         5: 16 * s,                  # Step 5: gather s splitters
         6: 4 * n + 8 * s * m + 4 * ms,  # Step 6: key reload, splitters per CTA, counts
         7: 12 * ms,                 # Step 7: read a twice, write l
-        8: 8 * n + 8 * ms,          # Step 8: read + write every key, a and l rows
-        9: 8 * n + 4 * s,           # Step 9: read + write every key
+        8: 2 * ib * n + 8 * ms,     # Step 8: read + write every item, a and l rows
+        9: None if nested else 2 * ib * n + 4 * s,   # Step 9: read + write every item
     }
 
 
@@ -182,19 +184,24 @@ def run_reference(args):
 # ----------------------------------------------------------------- GPU arm
 
 def cpu_baseline_line(args, n):
-    """The oracle as it stands, single-threaded, on the full workload once (~15 s)."""
+    """The oracle as it stands, single-threaded, once on a bounded sample of the workload
+    (the full C2 workload, ~10-15 s; C3/C4 are sampled at 2^25 items)."""
     import numpy as np
     import gbs_inputs as gi
     import oracle
     sys.path.insert(0, os.path.join(ROOT, "tests"))
-    from plans import plan as plan_rule
-    keys = gi.generate(args.dist, n, seed=0)
+    from plans import TILE_KEYS, TILE_PAIRS, plan as plan_rule
+    pairs = args.workload == "C4"
+    ns = min(n, 1 << 25)
+    keys = gi.generate(args.dist, ns, seed=0)
+    vals = gi.pair_values(ns) if pairs else None
     t0 = time.perf_counter()
-    oracle.gbs_sort(keys, plan=plan_rule(n))
+    oracle.gbs_sort(keys, vals, plan=plan_rule(ns, TILE_PAIRS if pairs else TILE_KEYS))
     dt = time.perf_counter() - t0
-    return {"value": n / dt, "unit": "keys/s", "cores": 1, "kind": "oracle",
-            "sample": f"one full {args.workload} sort ({n} keys, {args.dist}) by the single-threaded C "
-                      f"oracle, {dt:.1f} s"}
+    what = "full" if ns == n else f"2^{ns.bit_length() - 1}-item sample of the"
+    return {"value": ns / dt, "unit": "keys/s", "cores": 1, "kind": "oracle",
+            "sample": f"one {what} {args.workload} sort ({ns} {'pairs' if pairs else 'keys'}, {args.dist}) "
+                      f"by the single-threaded C oracle, {dt:.1f} s"}
 
 
 def main():
@@ -229,7 +236,12 @@ def main():
         pristine = gi.generate_torch("sorted", n * world, seed=0, device=dev)[n * rank:n * (rank + 1)].clone()
     else:
         pristine = gi.generate_torch(args.dist, n * world, seed=0, device=dev, start=n * rank, count=n)
+    pairs = args.workload == "C4"
+    if pairs and world > 1:
+        raise SystemExit("the multi-GPU entry sorts keys (DESIGN.md 7); C4 is a single-GPU workload")
     keys = torch.empty_like(pristine)
+    vals = torch.empty_like(pristine) if pairs else None
+    pristine_v = torch.arange(n, dtype=torch.int32, device=dev) if pairs else None
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
     ws = gbs.Workspace(dev)
     comm = gbs.Comm() if world > 1 else None
@@ -237,24 +249,40 @@ def main():
     if comm is not None:
         _, cap = gbs.dist_workspace_size(n, world)
         out = torch.empty(cap, dtype=torch.int32, device=dev)
-    plan = gbs.plan(n)
+    plan = gbs.plan(n, pairs=pairs)
+
+    def restore():
+        keys.copy_(pristine)
+        if pairs:
+            vals.copy_(pristine_v)
 
     def one_sort():
-        if comm is None:
+        if pairs:
+            gbs.sort_pairs(keys, vals, ws=ws)
+        elif comm is None:
             gbs.sort_keys(keys, ws=ws)
         else:
             gbs.sort_keys_dist(keys, comm, out=out, ws=ws)
 
     for _ in range(args.warmup):
-        keys.copy_(pristine)
+        restore()
         one_sort()
     torch.cuda.synchronize()
     # correctness of the timed configuration (single GPU): compare with the plain definition
     if comm is None:
-        keys.copy_(pristine)
+        restore()
         one_sort()
-        ref = torch.sort(pristine.to(torch.int64) & 0xFFFFFFFF).values
-        assert torch.equal(keys.to(torch.int64) & 0xFFFFFFFF, ref), "sort mismatch"
+        if pairs:   # stable: keys_out == keys_in[vals_out], nondecreasing, ties by position
+            k64 = keys.to(torch.int64) & 0xFFFFFFFF
+            assert torch.equal(pristine[vals.long()], keys), "pairs mismatch"
+            assert bool((k64[1:] >= k64[:-1]).all()), "pairs not sorted"
+            eq = k64[1:] == k64[:-1]
+            assert bool((vals[1:][eq] > vals[:-1][eq]).all()), "pairs not stable"
+            del k64, eq
+        else:
+            ref = torch.sort(pristine.to(torch.int64) & 0xFFFFFFFF).values
+            assert torch.equal(keys.to(torch.int64) & 0xFFFFFFFF, ref), "sort mismatch"
+            del ref
 
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -265,7 +293,7 @@ def main():
         gbs.profile_begin()
     with ClockSampler(local) as clk:
         for i in range(args.steps):
-            keys.copy_(pristine)
+            restore()
             flush.zero_()                                   # L2 flush (256 MiB > 126 MB L2)
             starts[i].record(stream)
             one_sort()
@@ -285,7 +313,7 @@ def main():
 
     # ---- end to end through the C-ABI with host buffers (N = 1)
     e2e = None
-    if comm is None:
+    if comm is None and not pairs:
         host = pristine.cpu().pin_memory()
         hbuf = torch.empty_like(host).pin_memory()
         dbuf = torch.empty_like(keys)
@@ -316,14 +344,14 @@ def main():
     steps = None
     if prof is not None and prof["calls"]:
         calls = prof["calls"]
-        ab = algorithmic_bytes(n, plan)
+        ab = algorithmic_bytes(n, plan, 8 if pairs else 4)
         steps = {}
         for k in (2, 4, 5, 6, 7, 8, 9):
             t_ms = prof[k] / calls
             gbps = (ab[k] / (t_ms / 1e3) / 1e9) if ab[k] and t_ms > 0 else None
             steps[STEP_NAMES[k]] = {"ms": round(t_ms, 4), "share": round(prof[k] / sum(prof[j] for j in (2, 4, 5, 6, 7, 8, 9)), 3),
                                     "alg_bytes": ab[k], "alg_GBps": round(gbps, 1) if gbps else None}
-        dom = max((2, 9, 8, 6), key=lambda k: prof[k])
+        dom = max((k for k in (2, 9, 8, 6) if ab[k]), key=lambda k: prof[k])
         t_ms = prof[dom] / calls
         ach = ab[dom] / (t_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "kernel": STEP_NAMES[dom], "achieved": round(ach, 1), "peak": peak,
@@ -337,7 +365,7 @@ def main():
 
     line = {"metric": METRIC, "value": value, "unit": "keys/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "vs_baseline": None, "dtype": "u32 pairs" if pairs else "u32", "data": "synthetic",
             "config": {"workload": wl, "n_per_gpu": n, "dist": args.dist,
                        "plan": plan["levels"], "bucket_bound": plan["bucket_bound"],
                        "l2": "flushed between steps (256 MiB memset) outside the event window",

@@ -70,17 +70,20 @@ struct BatcherNet {
     }
 };
 
-template <typename T, int N, size_t... Cs>
-__device__ __forceinline__ void apply_net(T (&x)[N], std::index_sequence<Cs...>)
+// Sorts x[0..N) of a register array of M >= N entries (a larger array lets one set of
+// registers serve several tile sizes).
+template <typename T, int N, int M, size_t... Cs>
+__device__ __forceinline__ void apply_net(T (&x)[M], std::index_sequence<Cs...>)
 {
     constexpr BatcherNet<N> net{};
     (cas(x[net.a[Cs]], x[net.b[Cs]]), ...);
 }
 
-template <typename T, int N>
-__device__ __forceinline__ void reg_sort(T (&x)[N])
+template <typename T, int N, int M>
+__device__ __forceinline__ void reg_sort(T (&x)[M])
 {
-    if constexpr (N > 1) apply_net<T, N>(x, std::make_index_sequence<BatcherNet<N>::C>{});
+    static_assert(N <= M, "register array too small");
+    if constexpr (N > 1) apply_net<T, N, M>(x, std::make_index_sequence<BatcherNet<N>::C>{});
 }
 
 #ifndef GBS_PAD_SHIFT
@@ -135,8 +138,10 @@ struct CtaSort {
     // An exhausted run reads as TMAX ("sticky sentinel"): for keys a tie between a
     // real 0xFFFFFFFF and the sentinel outputs the same value; u64 items never equal
     // TMAX.  Ties take A first, so the merge is stable.
-    static __device__ __forceinline__ void merge_thread(T (&x)[ITEMS], const T* sm, int start, int w)
+    template <int M>
+    static __device__ __forceinline__ void merge_thread(T (&x)[M], const T* sm, int start, int w)
     {
+        static_assert(M >= ITEMS, "register array too small");
         constexpr int H = ITEMS / CHAINS;
         const int base = start & ~(2 * w - 1);
         const int aEnd = base + w, bEnd = base + 2 * w;
@@ -194,24 +199,20 @@ struct CtaSort {
     // into shared memory (phys layout, TMAX beyond valid) and run only the merge levels
     // w = R, 2R, ... .  Used for Step 4, whose input is m sorted runs of s samples
     // (each sublist's samples come out of its sorted sublist).  Block-synchronised.
-    template <typename Src>
-    static __device__ __forceinline__ void sort_presorted(Src src, T* sm, int valid, int R)
+    template <int M, typename Src>
+    static __device__ __forceinline__ void sort_presorted(T (&x)[M], Src src, T* sm, int valid, int R)
     {
         const int t = threadIdx.x;
-        {
-            T y[ITEMS];
 #pragma unroll
-            for (int k = 0; k < ITEMS; ++k) {
-                const int p = t + k * BLOCK;
-                y[k] = p < valid ? src[p] : TMAX;
-            }
-#pragma unroll
-            for (int k = 0; k < ITEMS; ++k) sm[phys(t + k * BLOCK)] = y[k];
+        for (int k = 0; k < ITEMS; ++k) {
+            const int p = t + k * BLOCK;
+            x[k] = p < valid ? src[p] : TMAX;
         }
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k) sm[phys(t + k * BLOCK)] = x[k];
         __syncthreads();
         const int start = t * ITEMS;
         const int wspan0 = (t >> 5) * WARP_SPAN;
-        T x[ITEMS];
 #pragma unroll 1
         for (int w = R; w < TILE; w *= 2) {
             const bool intra = 2 * w <= WARP_SPAN;
@@ -228,13 +229,24 @@ struct CtaSort {
         }
     }
 
+    // Load x[0..ITEMS) with the positions load_pos(k) of src[0, valid) (coalesced:
+    // 32 consecutive per warp instruction); TMAX beyond valid.
+    template <int M, typename Src>
+    static __device__ __forceinline__ void load(T (&x)[M], Src src, int valid)
+    {
+        const int p0 = load_pos(0), rem = valid - p0;     // load_pos(k) = p0 + 32k
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k) x[k] = 32 * k < rem ? (T)src[p0 + 32 * k] : TMAX;
+    }
+
     // Sort: x[] holds the items of positions load_pos(k) (sentinels at >= valid).
     // On return sm[phys(p)] holds the sorted tile for p < valid (block-synchronised).
-    static __device__ __forceinline__ void sort(T (&x)[ITEMS], T* sm, int valid)
+    template <int M>
+    static __device__ __forceinline__ void sort(T (&x)[M], T* sm, int valid)
     {
         const int t = threadIdx.x;
         const int wspan0 = (t >> 5) * WARP_SPAN;
-        if (wspan0 < valid) reg_sort<T, ITEMS>(x);
+        if (wspan0 < valid) reg_sort<T, ITEMS, M>(x);
         const int start = t * ITEMS;
 #pragma unroll 1
         for (int w = ITEMS; w < TILE; w *= 2) {

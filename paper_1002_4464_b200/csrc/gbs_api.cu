@@ -10,6 +10,7 @@
 #include <array>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <type_traits>
@@ -41,12 +42,21 @@ static gbs_status_t fail(gbs_status_t st, const char* fmt, ...)
                         __FILE__, __LINE__);                                               \
     } while (0)
 
+// GBS_DEBUG_SYNC=1 in the environment: synchronise after every launch so a device fault
+// is attributed to its launch site (debugging only; never set in benchmarks).
+static bool debug_sync()
+{
+    static const bool on = getenv("GBS_DEBUG_SYNC") != nullptr;
+    return on;
+}
+
 #define GBS_LAUNCHED()                                                                     \
     do {                                                                                   \
         cudaError_t e_ = cudaGetLastError();                                               \
+        if (e_ == cudaSuccess && debug_sync()) e_ = cudaDeviceSynchronize();               \
         if (e_ != cudaSuccess)                                                             \
-            return fail(GBS_ERROR_CUDA, "kernel launch: %s (%s:%d)", cudaGetErrorString(e_), \
-                        __FILE__, __LINE__);                                               \
+            return fail(GBS_ERROR_CUDA, "kernel launch: %s (%s:%d, node kind %d B %u)",     \
+                        cudaGetErrorString(e_), __FILE__, __LINE__, KIND, nd.B);           \
     } while (0)
 
 // ----------------------------------------------------------------- step profiling
@@ -159,7 +169,7 @@ static int build_node(Plan& P, int kind, uint32_t B, uint64_t N, uint32_t pad_ba
         nd.o_reloc = P.alloc((uint64_t)B * N * key_bytes(kind));
         if (kind == KIND_PAIRS) nd.o_reloc_v = P.alloc((uint64_t)B * N * 4);
     }
-    P.launches += 5;  // local sort, global samples, sample index, scan, relocate
+    P.launches += 4;  // local sort (+samples), sample index (+splitters), scan, relocate
     const int idx = (int)P.nodes.size();
     P.nodes.push_back(nd);
     const uint32_t child_pad = kind == KIND_U64 ? pad_base + (uint32_t)(nd.Np - N) : (uint32_t)nd.Np;
@@ -199,6 +209,8 @@ static gbs_status_t make_plan(size_t n, int kind, const gbs_config_t* cfg, Plan&
 }
 
 // ----------------------------------------------------------------- launches
+static uint32_t num_sms();
+
 template <typename K>
 static void set_smem(K kernel, size_t bytes)
 {
@@ -206,20 +218,35 @@ static void set_smem(K kernel, size_t bytes)
 }
 
 template <int KIND, int BLOCK, int ITEMS>
-static void launch_local_t(const LevelDev& lv, cudaStream_t st)
+static void launch_local_t(const LevelDev& lv0, cudaStream_t st)
 {
     const size_t sm = Seg<KIND, BLOCK, ITEMS>::smem_bytes();
     static std::once_flag f;
-    std::call_once(f, [&] { set_smem(k_local_sort<KIND, BLOCK, ITEMS>, sm); });
-    k_local_sort<KIND, BLOCK, ITEMS><<<lv.B * lv.m, BLOCK, sm, st>>>(lv);
+    static int occ = 1;
+    std::call_once(f, [&] {
+        set_smem(k_local_sort<KIND, BLOCK, ITEMS>, sm);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_local_sort<KIND, BLOCK, ITEMS>, BLOCK, sm) !=
+                cudaSuccess || occ < 1)
+            occ = 1;
+    });
+    // persistent: one CTA per resident slot, each walks tiles blockIdx.x + k*gridDim.x
+    const unsigned grid = std::min<unsigned>(lv0.B * lv0.m, num_sms() * (unsigned)occ);
+    k_local_sort<KIND, BLOCK, ITEMS><<<grid, BLOCK, sm, st>>>(lv0);
 }
 
 template <int KIND, int BLOCK, int ITEMS, int MODE>
-static void launch_seg_t(const LevelDev& lv, unsigned grid, cudaStream_t st)
+static void launch_seg_t(const LevelDev& lv, unsigned count, cudaStream_t st)
 {
     const size_t sm = Seg<KIND, BLOCK, ITEMS>::smem_bytes();
     static std::once_flag f;
-    std::call_once(f, [&] { set_smem(k_segment_sort<KIND, BLOCK, ITEMS, MODE>, sm); });
+    static int occ = 1;
+    std::call_once(f, [&] {
+        set_smem(k_segment_sort<KIND, BLOCK, ITEMS, MODE>, sm);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_segment_sort<KIND, BLOCK, ITEMS, MODE>, BLOCK,
+                                                          sm) != cudaSuccess || occ < 1)
+            occ = 1;
+    });
+    const unsigned grid = std::min<unsigned>(count, num_sms() * (unsigned)occ);
     k_segment_sort<KIND, BLOCK, ITEMS, MODE><<<grid, BLOCK, sm, st>>>(lv);
 }
 
@@ -258,7 +285,8 @@ static void launch_seg(const LevelDev& lv, bool small, unsigned grid, cudaStream
 template <int KIND>
 static void launch_index(const LevelDev& lv, cudaStream_t st)
 {
-    const size_t sm = (size_t)lv.s * 8 + (size_t)(lv.s + (lv.s & 1)) * 4 + (size_t)lv.L * key_bytes(KIND);
+    const size_t chunk = std::min<size_t>((size_t)lv.L * key_bytes(KIND), IDX_CHUNK_BYTES);
+    const size_t sm = (size_t)lv.s * 8 + (size_t)(lv.s + (lv.s & 1)) * 4 + chunk;
     static std::once_flag f;
     std::call_once(f, [&] { set_smem(k_sample_index<KIND, IDX_BLOCK>, 227 * 1024); });
     k_sample_index<KIND, IDX_BLOCK><<<lv.B * lv.m, IDX_BLOCK, sm, st>>>(lv);
@@ -268,7 +296,8 @@ template <int KIND>
 static void launch_relocate(const LevelDev& lv, cudaStream_t st)
 {
     constexpr int MAXPER = (int)(tile_of_c(KIND) / IDX_BLOCK);
-    const size_t sm = ((size_t)2 * lv.s + lv.L + IDX_BLOCK + 1) * 4;
+    const size_t per = std::max<size_t>(1, lv.L / IDX_BLOCK);
+    const size_t sm = (size_t)2 * lv.s * 4 + (lv.L + 2 * (lv.L / per) + 4) * 2;
     static std::once_flag f;
     std::call_once(f, [&] { set_smem(k_relocate<KIND, IDX_BLOCK, MAXPER>, 220 * 1024); });
     k_relocate<KIND, IDX_BLOCK, MAXPER><<<lv.B * lv.m, IDX_BLOCK, sm, st>>>(lv);
@@ -362,18 +391,34 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
     if (stop == 4) return GBS_SUCCESS;
     pm.mark();
 
-    // Step 5: global samples
-    {
+    // Step 5 (global samples) is fused into Step 6's prologue; the stand-alone kernel
+    // runs only when a caller stops right after Step 5 (stage parity).
+    if (stop == 5) {
         const uint64_t tot = (uint64_t)nd.B * nd.s;
         k_global_samples<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(lv);
         GBS_LAUNCHED();
+        return GBS_SUCCESS;
     }
-    if (stop == 5) return GBS_SUCCESS;
     pm.mark();
 
-    // Step 6: sample indexing -> a
+    // Steps 5-6: sample indexing -> a
     launch_index<KIND>(lv, st);
     GBS_LAUNCHED();
+    if (debug_sync()) {   // invariants of Steps 4 and 6 (debugging only)
+        unsigned* dflag = nullptr;
+        GBS_CUDA(cudaMallocManaged(&dflag, 8 * sizeof(unsigned)));
+        memset(dflag, 0, 8 * sizeof(unsigned));
+        k_check_level<<<1024, 256, 0, st>>>(lv, dflag);
+        GBS_CUDA(cudaStreamSynchronize(st));
+        unsigned fl[8];
+        memcpy(fl, dflag, sizeof fl);
+        cudaFree(dflag);
+        if (fl[0])
+            return fail(GBS_ERROR_CUDA, "invariant check failed (flag %u: 1 = samples unsorted, 2 = a rows) at node "
+                        "%d kind %d B %u N %llu L %u s %u m %u; first bad row b %u i %u sum %u v %u len %u "
+                        "g_last %08x:%08x", fl[0], ni, KIND, nd.B, (unsigned long long)nd.N, nd.L, nd.s, nd.m,
+                        fl[1], fl[2], fl[3], fl[4], fl[5], fl[6], fl[7]);
+    }
     if (stop == 6) return GBS_SUCCESS;
     pm.mark();
 

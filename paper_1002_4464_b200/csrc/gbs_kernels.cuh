@@ -140,8 +140,9 @@ __device__ __forceinline__ unsigned long long pad64(uint32_t pad_base, uint64_t 
 }
 
 // ------------------------------------------------------------------ segment I/O
-// Sort `v` items starting at element offset `src_off` of lv.in-like buffer `src`
-// and leave the sorted tile in shared memory (pairs: values staged in vsm).
+// One tile of `v` items at element offset `off` of an HBM buffer: registers <- HBM
+// (load_regs), on-chip sort (CS::sort, result in shared memory), HBM <- shared memory
+// (store).  Pairs sort (key << 32 | position) and stage the values in vsm.
 template <int KIND, int BLOCK, int ITEMS>
 struct Seg {
     using T = typename ItemT<KIND>::T;
@@ -152,42 +153,40 @@ struct Seg {
     {
         return sizeof(T) * CS::SMEM_ELEMS + (KIND == KIND_PAIRS ? sizeof(uint32_t) * TILE : 0);
     }
-
-    static __device__ __forceinline__ void load_sort(const void* src, const uint32_t* src_v, uint64_t src_off,
-                                                     int v, T* sm, uint32_t* vsm)
+    static __device__ __forceinline__ uint32_t* vsm_of(unsigned char* smem)
     {
-        T x[ITEMS];
-        if constexpr (KIND == KIND_KEYS) {
-            const int p0 = CS::load_pos(0), rem = v - p0;    // load_pos(k) = p0 + 32k
-            const uint32_t* s = reinterpret_cast<const uint32_t*>(src) + src_off + p0;
-#pragma unroll
-            for (int k = 0; k < ITEMS; ++k) x[k] = 32 * k < rem ? (T)__ldg(s + 32 * k) : (T)0xFFFFFFFFu;
-        } else if constexpr (KIND == KIND_PAIRS) {
+        return reinterpret_cast<uint32_t*>(reinterpret_cast<T*>(smem) + CS::SMEM_ELEMS);
+    }
+
+    template <int M>
+    static __device__ __forceinline__ void load_regs(T (&x)[M], const void* src, const uint32_t* src_v,
+                                                     uint64_t off, int v, unsigned char* smem)
+    {
+        if constexpr (KIND == KIND_PAIRS) {
             const int p0 = CS::load_pos(0), rem = v - p0;
-            const uint32_t* s = reinterpret_cast<const uint32_t*>(src) + src_off + p0;
-            const uint32_t* sv = src_v + src_off;
+            const uint32_t* s = reinterpret_cast<const uint32_t*>(src) + off + p0;
 #pragma unroll
             for (int k = 0; k < ITEMS; ++k) {
                 const uint32_t key = 32 * k < rem ? __ldg(s + 32 * k) : 0xFFFFFFFFu;
                 x[k] = ((T)key << 32) | (T)(uint32_t)(p0 + 32 * k);     // stable: ties by position
             }
+            uint32_t* vsm = vsm_of(smem);
+            const uint32_t* sv = src_v + off;
             for (int p = threadIdx.x; p < v; p += BLOCK) vsm[p] = __ldg(sv + p);
         } else {
-            const int p0 = CS::load_pos(0), rem = v - p0;
-            const unsigned long long* s = reinterpret_cast<const unsigned long long*>(src) + src_off + p0;
-#pragma unroll
-            for (int k = 0; k < ITEMS; ++k) x[k] = 32 * k < rem ? (T)__ldg(s + 32 * k) : (T)~0ull;
+            CS::load(x, reinterpret_cast<const KeyT*>(src) + off, v);
         }
-        CS::sort(x, sm, v);
     }
 
     static __device__ __forceinline__ void store(void* dst, uint32_t* dst_v, uint64_t dst_off, int v,
-                                                 const T* sm, const uint32_t* vsm)
+                                                 unsigned char* smem)
     {
+        const T* sm = reinterpret_cast<const T*>(smem);
         if constexpr (KIND == KIND_KEYS) {
             uint32_t* d = reinterpret_cast<uint32_t*>(dst) + dst_off;
             for (int p = threadIdx.x; p < v; p += BLOCK) d[p] = (uint32_t)sm[CS::phys(p)];
         } else if constexpr (KIND == KIND_PAIRS) {
+            const uint32_t* vsm = vsm_of(smem);
             uint32_t* d = reinterpret_cast<uint32_t*>(dst) + dst_off;
             uint32_t* dv = dst_v + dst_off;
             for (int p = threadIdx.x; p < v; p += BLOCK) {
@@ -202,58 +201,115 @@ struct Seg {
     }
 };
 
+// The same CTA sorts a tile of v items with ITEMS, ITEMS/2 or ITEMS/4 items per thread
+// -- the smallest that holds v (block-uniform choice) -- so every thread stays busy: a
+// bucket of half the capacity (the average, the bound being ~2n/s) costs about half.
+// One register array of ITEMS entries serves every size.
+template <int KIND, int BLOCK, int ITEMS, int DEPTH>
+struct Adapt {
+    using S = Seg<KIND, BLOCK, ITEMS>;
+    using T = typename S::T;
+    static constexpr bool HALF = DEPTH > 0 && ITEMS >= 8;
+    using Sub = Adapt<KIND, BLOCK, (HALF ? ITEMS / 2 : ITEMS), (HALF ? DEPTH - 1 : 0)>;
+
+    template <int M>
+    static __device__ __forceinline__ void load(T (&x)[M], const void* src, const uint32_t* src_v, uint64_t off,
+                                                int v, unsigned char* smem)
+    {
+        if constexpr (HALF) {
+            if (v <= S::TILE / 2) { Sub::load(x, src, src_v, off, v, smem); return; }
+        }
+        S::load_regs(x, src, src_v, off, v, smem);
+    }
+    template <int M>
+    static __device__ __forceinline__ void sort(T (&x)[M], unsigned char* smem, int v)
+    {
+        if constexpr (HALF) {
+            if (v <= S::TILE / 2) { Sub::sort(x, smem, v); return; }
+        }
+        S::CS::sort(x, reinterpret_cast<T*>(smem), v);
+    }
+    static __device__ __forceinline__ void store(void* dst, uint32_t* dst_v, uint64_t off, int v, unsigned char* smem)
+    {
+        if constexpr (HALF) {
+            if (v <= S::TILE / 2) { Sub::store(dst, dst_v, off, v, smem); return; }
+        }
+        S::store(dst, dst_v, off, v, smem);
+    }
+};
+
 // ------------------------------------------------------------ Steps 2 + 3
 // Step 2: sort sublist A_i of problem b in place.  Step 3,
 // fused into the write-back as the paper does: s samples at sorted
 // positions (k+1)d - 1 (R2), as composites (key << 32 | tag), tag = iL + r (R3).
+// Persistent CTAs (grid = SMs x CTAs/SM) walk the sublists; for keys and u64 the next
+// sublist is loaded into registers while the current one is written back (software
+// pipelining: the HBM load latency hides behind the store phase), and it is
+// prefetched into L2 one sublist ahead.
 template <int KIND, int BLOCK, int ITEMS>
 __global__ void __launch_bounds__(BLOCK, 1) k_local_sort(LevelDev lv)
 {
     using S = Seg<KIND, BLOCK, ITEMS>;
     using T = typename S::T;
+    using KeyT = typename S::KeyT;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T* sm = reinterpret_cast<T*>(smem_raw);
-    uint32_t* vsm = reinterpret_cast<uint32_t*>(sm + S::CS::SMEM_ELEMS);
 
-    const uint32_t b = blockIdx.x / lv.m, i = blockIdx.x % lv.m;
-    const uint64_t off = lv.pr.offset(b);
-    const uint32_t len = lv.pr.length(b);
-    const uint64_t i0 = (uint64_t)i * lv.L;
-    const int v = len > i0 ? (int)umin64(len - i0, lv.L) : 0;
-
-    if (threadIdx.x == 0 && blockIdx.x + lv.pf_stride < lv.B * lv.m) {
-        uint64_t ps;
-        int pv;
-        sublist_of(lv, blockIdx.x + lv.pf_stride, ps, pv);
-        prefetch_l2(reinterpret_cast<const char*>(lv.in) + ps * sizeof(typename S::KeyT), (size_t)pv * sizeof(typename S::KeyT));
-        if (KIND == KIND_PAIRS) prefetch_l2(lv.in_v + ps, (size_t)pv * 4);
+    const uint32_t ntiles = lv.B * lv.m;
+    const bool presorted = KIND == KIND_U64 && GBS_PRESORTED && lv.presorted >= (uint32_t)ITEMS;
+    const bool pipe = KIND != KIND_PAIRS && !presorted;
+    T x[ITEMS];
+    uint32_t tile = blockIdx.x;
+    uint64_t start = 0;
+    int v = 0;
+    if (tile < ntiles) {
+        sublist_of(lv, tile, start, v);
+        if (pipe) S::load_regs(x, lv.in, lv.in_v, start, v, smem_raw);
     }
-    if (v > 0) {
-        bool done = false;
-        if constexpr (KIND == KIND_U64) {
-            if (GBS_PRESORTED && lv.presorted >= (uint32_t)ITEMS) {
-                const unsigned long long* src = reinterpret_cast<const unsigned long long*>(lv.in) + off + i0;
-                S::CS::sort_presorted(src, sm, v, (int)lv.presorted);
-                done = true;
+    for (; tile < ntiles; tile += gridDim.x) {
+        const uint32_t b = tile / lv.m, i = tile % lv.m;
+        const uint32_t len = lv.pr.length(b);
+        const uint64_t i0 = (uint64_t)i * lv.L;
+        const uint32_t nxt = tile + gridDim.x;
+        uint64_t nstart = 0;
+        int nv = 0;
+        if (nxt < ntiles) {
+            sublist_of(lv, nxt, nstart, nv);
+            if (threadIdx.x == 0) {
+                prefetch_l2(reinterpret_cast<const KeyT*>(lv.in) + nstart, (size_t)nv * sizeof(KeyT));
+                if (KIND == KIND_PAIRS) prefetch_l2(lv.in_v + nstart, (size_t)nv * 4);
             }
         }
-        if (!done) S::load_sort(lv.in, lv.in_v, off + i0, v, sm, vsm);
-        S::store(lv.in, lv.in_v, off + i0, v, sm, vsm);
-    }
-    u64* smp = lv.samples + ((uint64_t)b * lv.m + i) * lv.s;
-    for (uint32_t k = threadIdx.x; k < lv.s; k += BLOCK) {
-        const uint32_t r = (k + 1) * lv.d - 1;
-        const uint32_t tag = (uint32_t)i0 + r;
-        unsigned long long c;
-        if (KIND == KIND_U64) {
-            c = (int)r < v ? (unsigned long long)sm[S::CS::phys(r)] : pad64(lv.pad_base, i0 + r - len);
-        } else {
-            uint32_t key = 0xFFFFFFFFu;
-            if ((int)r < v) key = KIND == KIND_KEYS ? (uint32_t)sm[S::CS::phys(r)]
-                                                    : (uint32_t)((unsigned long long)sm[S::CS::phys(r)] >> 32);
-            c = ((unsigned long long)key << 32) | tag;
+        if (v > 0) {
+            if (presorted) {
+                if constexpr (KIND == KIND_U64)
+                    S::CS::sort_presorted(x, reinterpret_cast<const unsigned long long*>(lv.in) + start, sm, v,
+                                          (int)lv.presorted);
+            } else {
+                if (!pipe) S::load_regs(x, lv.in, lv.in_v, start, v, smem_raw);
+                S::CS::sort(x, sm, v);
+            }
         }
-        smp[k] = c;
+        if (pipe && nv > 0) S::load_regs(x, lv.in, lv.in_v, nstart, nv, smem_raw);   // in flight during the store
+        if (v > 0) S::store(lv.in, lv.in_v, start, v, smem_raw);
+        u64* smp = lv.samples + ((uint64_t)b * lv.m + i) * lv.s;
+        for (uint32_t k = threadIdx.x; k < lv.s; k += BLOCK) {
+            const uint32_t r = (k + 1) * lv.d - 1;
+            const uint32_t tag = (uint32_t)i0 + r;
+            unsigned long long c;
+            if (KIND == KIND_U64) {
+                c = (int)r < v ? (unsigned long long)sm[S::CS::phys(r)] : pad64(lv.pad_base, i0 + r - len);
+            } else {
+                uint32_t key = 0xFFFFFFFFu;
+                if ((int)r < v) key = KIND == KIND_KEYS ? (uint32_t)sm[S::CS::phys(r)]
+                                                        : (uint32_t)((unsigned long long)sm[S::CS::phys(r)] >> 32);
+                c = ((unsigned long long)key << 32) | tag;
+            }
+            smp[k] = c;
+        }
+        __syncthreads();                     // shared memory is reused by the next sublist
+        start = nstart;
+        v = nv;
     }
 }
 
@@ -274,8 +330,10 @@ __global__ void k_global_samples(LevelDev lv)
 // (the paper loads the s global samples into shared memory); each thread
 // bisects for its splitters -- the paper's staged schedule only avoided
 // GT200 bank contention and does not change the result (R10).
+static constexpr int IDX_CHUNK_BYTES = 64 * 1024;
+
 template <int KIND, int BLOCK>
-__global__ void __launch_bounds__(BLOCK) k_sample_index(LevelDev lv)
+__global__ void __launch_bounds__(BLOCK, 2) k_sample_index(LevelDev lv)
 {
     using KT = typename std::conditional<KIND == KIND_U64, unsigned long long, uint32_t>::type;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -296,23 +354,46 @@ __global__ void __launch_bounds__(BLOCK) k_sample_index(LevelDev lv)
         sublist_of(lv, blockIdx.x + lv.pf_stride, ps, pv);
         prefetch_l2(reinterpret_cast<const KT*>(lv.in) + ps, (size_t)pv * sizeof(KT));
     }
-    stage_to_smem<BLOCK>(ks, src, (size_t)v * sizeof(KT));
-    const unsigned long long* g = lv.splitters + (uint64_t)b * lv.s;
-    for (uint32_t j = threadIdx.x; j < lv.s; j += BLOCK) gs[j] = g[j];
-    __syncthreads();
+    // Step 5 fused into the prologue (the paper loads the s global samples into shared
+    // memory here): g_j = sorted_samples[(j+1)m - 1]; sublist 0 of each
+    // problem also records them (the splitters array, for stage parity).
+    const u64* srt = lv.samples + (uint64_t)b * lv.m * lv.s;
     for (uint32_t j = threadIdx.x; j < lv.s; j += BLOCK) {
-        const unsigned long long gj = gs[j];
-        int lo = 0, hi = v;
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            unsigned long long rk;
-            if (KIND == KIND_U64) rk = (unsigned long long)ks[mid];
-            else rk = ((unsigned long long)ks[mid] << 32) | (uint32_t)(i0 + mid);
-            if (rk <= gj) lo = mid + 1; else hi = mid;
-        }
-        Q[j] = (uint32_t)lo;
+        const u64 gj = srt[(uint64_t)(j + 1) * lv.m - 1];
+        gs[j] = gj;
+        Q[j] = 0;
+        if (i == 0) lv.splitters[(uint64_t)b * lv.s + j] = gj;
     }
-    __syncthreads();
+    // The sublist is searched in chunks of IDX_CHUNK bytes (64 KB) so the CTA fits
+    // twice per SM: one CTA's chunk load overlaps the other's bisections.  The
+    // count over the sublist is the sum of the counts over its sorted chunks.
+    constexpr int CH = IDX_CHUNK_BYTES / sizeof(KT);
+    for (int c0 = 0; c0 < v; c0 += CH) {
+        const int cl = min(CH, v - c0);
+        stage_to_smem<BLOCK>(ks, src + c0, (size_t)cl * sizeof(KT));
+        __syncthreads();
+        auto rank_key = [&](int q) -> unsigned long long {
+            if (KIND == KIND_U64) return (unsigned long long)ks[q];
+            return ((unsigned long long)ks[q] << 32) | (uint32_t)(i0 + c0 + q);
+        };
+        const unsigned long long first = rank_key(0), last = rank_key(cl - 1);
+        for (uint32_t j = threadIdx.x; j < lv.s; j += BLOCK) {
+            const unsigned long long gj = gs[j];
+            int lo = 0, hi = cl;
+            if (gj < first) hi = 0;                       // whole chunk above g_j
+            else if (gj >= last) lo = cl;                 // whole chunk at or below g_j
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                unsigned long long rk;
+                if (KIND == KIND_U64) rk = (unsigned long long)ks[mid];
+                else rk = ((unsigned long long)ks[mid] << 32) | (uint32_t)(i0 + c0 + mid);
+                if (rk <= gj) lo = mid + 1; else hi = mid;
+            }
+            Q[j] += (uint32_t)lo;
+        }
+        __syncthreads();
+    }
+    __syncthreads();   // Q complete (also when v == 0 and the chunk loop never ran)
     uint32_t* arow = lv.a + ((uint64_t)b * lv.m + i) * lv.s;
     for (uint32_t j = threadIdx.x; j < lv.s; j += BLOCK) arow[j] = Q[j] - (j ? Q[j - 1] : 0u);
 }
@@ -390,7 +471,18 @@ __global__ void __launch_bounds__(SCAN_BLOCK) k_scan(LevelDev lv)
     __syncthreads();
     if (col_ok) {
         uint32_t run = (uint32_t)blk_prefix + colpre[lane] + wsum[w][lane];
-        for (uint64_t r = r0; r < r1; ++r) {
+        uint64_t r = r0;
+        for (; r + 8 <= r1; r += 8) {           // 8 independent loads in flight
+            uint32_t x[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) x[u] = A[(r + u) * lv.s + c];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                Lo[(r + u) * lv.s + c] = run;
+                run += x[u];
+            }
+        }
+        for (; r < r1; ++r) {
             const uint32_t x = A[r * lv.s + c];
             Lo[r * lv.s + c] = run;
             run += x;
@@ -443,16 +535,16 @@ __device__ __forceinline__ int upper_bound_u32(const uint32_t* a, int lo, int hi
     return lo;
 }
 
-// MAXPER = max items per thread (L / BLOCK): the sublist is prefetched into registers
-// (striped, coalesced) while the destination map is built, then stored.
+// A u16 bucket map (bucket of every position) keeps the CTA at ~100 KB of shared
+// memory, so two CTAs share an SM and one's loads overlap the other's map build.
 template <int KIND, int BLOCK, int MAXPER>
-__global__ void __launch_bounds__(BLOCK, 1) k_relocate(LevelDev lv)
+__global__ void __launch_bounds__(BLOCK, 2) k_relocate(LevelDev lv)
 {
     using KT = typename std::conditional<KIND == KIND_U64, unsigned long long, uint32_t>::type;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint32_t* starts = reinterpret_cast<uint32_t*>(smem_raw);
     uint32_t* delta = starts + lv.s;
-    uint32_t* dest = delta + lv.s;          // L + BLOCK entries (one pad slot per `per`)
+    uint16_t* bmap = reinterpret_cast<uint16_t*>(delta + lv.s);   // L + 2L/per + 2 entries
     __shared__ uint32_t wtmp[32];
 
     const uint32_t b = blockIdx.x / lv.m, i = blockIdx.x % lv.m;
@@ -471,13 +563,6 @@ __global__ void __launch_bounds__(BLOCK, 1) k_relocate(LevelDev lv)
         prefetch_l2(reinterpret_cast<const KT*>(lv.in) + ps, (size_t)pv * sizeof(KT));
         if (KIND == KIND_PAIRS) prefetch_l2(lv.in_v + ps, (size_t)pv * 4);
     }
-    KT x[MAXPER];
-    {
-        const int rem = v - (int)threadIdx.x;
-        const KT* s0 = src + threadIdx.x;
-#pragma unroll
-        for (int k = 0; k < MAXPER; ++k) x[k] = k * BLOCK < rem ? s0[k * BLOCK] : KT(0);
-    }
 
     const uint64_t row = ((uint64_t)b * lv.m + i) * lv.s;
     for (uint32_t j = threadIdx.x; j < lv.s; j += BLOCK) starts[j] = lv.a[row + j];
@@ -486,40 +571,47 @@ __global__ void __launch_bounds__(BLOCK, 1) k_relocate(LevelDev lv)
     for (uint32_t j = threadIdx.x; j < lv.s; j += BLOCK) delta[j] = lv.l[row + j] - starts[j];
     __syncthreads();
 
-    // destination map: thread t walks positions [t*per, t*per + per) (blocked) and
-    // writes dest at r + r/per (padding keeps the blocked writes bank-conflict free)
+    // bucket map: thread t walks positions [t*per, t*per + per) (blocked), keeping the
+    // next bucket start in a register; the map entry of r lives at r + 2 r/per (u16
+    // units: each thread's row is 33 words, so the blocked writes are conflict free)
     const int S = (int)lv.s;
     const int per = (int)(lv.L / BLOCK) > 0 ? (int)(lv.L / BLOCK) : 1;   // power of two
     const int lp = 31 - __clz(per);
     const int r0 = threadIdx.x * per, r1 = min(v, r0 + per);
     if (r0 < r1) {
         int j = upper_bound_u32(starts, 0, S, (uint32_t)r0) - 1;
+        uint32_t nxt = j + 1 < S ? starts[j + 1] : 0xFFFFFFFFu;
         for (int r = r0; r < r1; ++r) {
-            if (j + 1 < S && starts[j + 1] <= (uint32_t)r) {
+            while ((uint32_t)r >= nxt) {          // crossed a bucket boundary (rare)
                 ++j;
-                if (j + 1 < S && starts[j + 1] <= (uint32_t)r) j = upper_bound_u32(starts, j + 1, S, (uint32_t)r) - 1;
+                nxt = j + 1 < S ? starts[j + 1] : 0xFFFFFFFFu;
             }
-            dest[r + (r >> lp)] = (uint32_t)r + delta[j];
+            bmap[r + 2 * (r >> lp)] = (uint16_t)j;
         }
     }
     __syncthreads();
     KT* dst = reinterpret_cast<KT*>(lv.reloc) + off;
+    for (int q0 = threadIdx.x; q0 < v; q0 += 8 * BLOCK) {
+        KT y[8];
 #pragma unroll
-    for (int k = 0; k < MAXPER; ++k) {
-        const int r = threadIdx.x + k * BLOCK;
-        if (r < v) dst[dest[r + (r >> lp)]] = x[k];
+        for (int u = 0; u < 8; ++u) y[u] = q0 + u * BLOCK < v ? src[q0 + u * BLOCK] : KT(0);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int r = q0 + u * BLOCK;
+            if (r < v) dst[(uint32_t)r + delta[bmap[r + 2 * (r >> lp)]]] = y[u];
+        }
     }
     if (KIND == KIND_PAIRS) {
         const uint32_t* sv = lv.in_v + off + i0;
         uint32_t* dv = lv.reloc_v + off;
-        uint32_t y[8];
-        for (int r0v = threadIdx.x; r0v < v; r0v += 8 * BLOCK) {
+        for (int q0 = threadIdx.x; q0 < v; q0 += 8 * BLOCK) {
+            uint32_t y[8];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) y[u] = r0v + u * BLOCK < v ? sv[r0v + u * BLOCK] : 0u;
+            for (int u = 0; u < 8; ++u) y[u] = q0 + u * BLOCK < v ? sv[q0 + u * BLOCK] : 0u;
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
-                const int r = r0v + u * BLOCK;
-                if (r < v) dv[dest[r + (r >> lp)]] = y[u];
+                const int r = q0 + u * BLOCK;
+                if (r < v) dv[(uint32_t)r + delta[bmap[r + 2 * (r >> lp)]]] = y[u];
             }
         }
     }
@@ -531,72 +623,95 @@ __global__ void __launch_bounds__(BLOCK, 1) k_relocate(LevelDev lv)
 // one CTA per whole problem (len_b <= tile).
 enum SegMode { MODE_BUCKET = 0, MODE_LEAF = 1 };
 
-// Sort v items with the smallest tile (ITEMS, ITEMS/2, ITEMS/4 per thread; same CTA)
-// that holds them: every thread stays busy, so a bucket of half the capacity (the
-// average, since the bound is ~2n/s) costs about half.  Block-uniform branch.
-template <int KIND, int BLOCK, int ITEMS, int DEPTH>
-__device__ __forceinline__ void seg_sort_adaptive(const void* src, const uint32_t* src_v, uint64_t off, int v,
-                                                  void* dst, uint32_t* dst_v, unsigned char* smem_raw)
+// Segment idx of a Step-9 / leaf launch: element offset and length.
+template <int MODE>
+__device__ __forceinline__ void segment_of(const LevelDev& lv, uint32_t idx, uint64_t& off, int& v)
 {
-    if constexpr (DEPTH > 0 && ITEMS >= 8) {
-        if (v <= BLOCK * ITEMS / 2) {
-            seg_sort_adaptive<KIND, BLOCK, ITEMS / 2, DEPTH - 1>(src, src_v, off, v, dst, dst_v, smem_raw);
-            return;
-        }
-    }
-    using S = Seg<KIND, BLOCK, ITEMS>;
-    using T = typename S::T;
-    T* sm = reinterpret_cast<T*>(smem_raw);
-    uint32_t* vsm = reinterpret_cast<uint32_t*>(sm + S::CS::SMEM_ELEMS);
-    S::load_sort(src, src_v, off, v, sm, vsm);
-    S::store(dst, dst_v, off, v, sm, vsm);
-}
-
-template <int KIND, int BLOCK, int ITEMS, int MODE>
-__global__ void __launch_bounds__(BLOCK, 1) k_segment_sort(LevelDev lv)
-{
-    using S = Seg<KIND, BLOCK, ITEMS>;
-    using T = typename S::T;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    T* sm = reinterpret_cast<T*>(smem_raw);
-    uint32_t* vsm = reinterpret_cast<uint32_t*>(sm + S::CS::SMEM_ELEMS);
-
-    uint32_t b;
-    uint64_t start;
-    int v;
-    const void* src;
-    const uint32_t* src_v;
     if (MODE == MODE_LEAF) {
-        b = blockIdx.x;
-        start = 0;
-        v = (int)lv.pr.length(b);
-        src = lv.in;
-        src_v = lv.in_v;
+        off = lv.pr.offset(idx);
+        v = (int)lv.pr.length(idx);
     } else {
-        b = blockIdx.x / lv.s;
-        const uint32_t j = blockIdx.x % lv.s;
+        const uint32_t b = idx / lv.s, j = idx % lv.s;
         const uint32_t* l0 = lv.l + (uint64_t)b * lv.m * lv.s;   // row 0 of problem b
         const uint32_t st = l0[j];
         const uint32_t en = j + 1 < lv.s ? l0[j + 1] : lv.pr.length(b);
-        start = st;
+        off = lv.pr.offset(b) + st;
         v = (int)(en - st);
-        src = lv.reloc;
-        src_v = lv.reloc_v;
-        const uint32_t nxt = blockIdx.x + lv.pf_stride;
-        if (threadIdx.x == 0 && nxt < lv.B * lv.s) {
-            const uint32_t nb = nxt / lv.s, nj = nxt % lv.s;
-            const uint32_t* n0 = lv.l + (uint64_t)nb * lv.m * lv.s;
-            const uint32_t ns = n0[nj], ne = nj + 1 < lv.s ? n0[nj + 1] : lv.pr.length(nb);
-            const uint64_t po = lv.pr.offset(nb) + ns;
-            prefetch_l2(reinterpret_cast<const typename S::KeyT*>(lv.reloc) + po, (size_t)(ne - ns) * sizeof(typename S::KeyT));
-            if (KIND == KIND_PAIRS) prefetch_l2(lv.reloc_v + po, (size_t)(ne - ns) * 4);
+    }
+}
+
+// Persistent CTAs walk the segments (buckets or leaf problems), adaptive tile size,
+// next segment loaded into registers during the current write-back (keys, u64).
+template <int KIND, int BLOCK, int ITEMS, int MODE>
+__global__ void __launch_bounds__(BLOCK, 1) k_segment_sort(LevelDev lv)
+{
+    using A = Adapt<KIND, BLOCK, ITEMS, GBS_ADAPT_DEPTH>;
+    using T = typename A::T;
+    using KeyT = typename A::S::KeyT;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr bool PIPE = KIND != KIND_PAIRS;
+    const void* src = MODE == MODE_LEAF ? lv.in : lv.reloc;
+    const uint32_t* src_v = MODE == MODE_LEAF ? lv.in_v : lv.reloc_v;
+    const uint32_t count = MODE == MODE_LEAF ? lv.B : lv.B * lv.s;
+
+    T x[ITEMS];
+    uint32_t cur = blockIdx.x;
+    uint64_t off = 0;
+    int v = 0;
+    if (cur < count) {
+        segment_of<MODE>(lv, cur, off, v);
+        if (PIPE && v > 0) A::load(x, src, src_v, off, v, smem_raw);
+    }
+    while (cur < count) {
+        const uint32_t nxt = cur + gridDim.x;
+        uint64_t noff = 0;
+        int nv = 0;
+        if (nxt < count) {
+            segment_of<MODE>(lv, nxt, noff, nv);
+            if (threadIdx.x == 0 && nv > 0) {
+                prefetch_l2(reinterpret_cast<const KeyT*>(src) + noff, (size_t)nv * sizeof(KeyT));
+                if (KIND == KIND_PAIRS) prefetch_l2(src_v + noff, (size_t)nv * 4);
+            }
+        }
+        if (v > 0) {
+            if (!PIPE) A::load(x, src, src_v, off, v, smem_raw);
+            A::sort(x, smem_raw, v);
+            if (PIPE && nv > 0) A::load(x, src, src_v, noff, nv, smem_raw);   // in flight during the store
+            A::store(lv.out, lv.out_v, off, v, smem_raw);
+            __syncthreads();
+        } else if (PIPE && nv > 0) {
+            A::load(x, src, src_v, noff, nv, smem_raw);
+        }
+        cur = nxt;
+        off = noff;
+        v = nv;
+    }
+}
+
+// Debug-only invariant checks (GBS_DEBUG_SYNC): *flag |= 1 if some problem's sorted
+// samples are out of order, |= 2 if some row of a does not sum to the sublist's
+// real item count (conservation).
+__global__ void k_check_level(LevelDev lv, unsigned* flag)
+{
+    const uint64_t ms = (uint64_t)lv.m * lv.s;
+    for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < (uint64_t)lv.B * ms;
+         q += (uint64_t)gridDim.x * blockDim.x) {
+        if (q % ms != 0 && lv.samples[q] <= lv.samples[q - 1]) atomicOr(flag, 1u);
+        if (q % lv.s == 0) {
+            const uint64_t row = q / lv.s;
+            const uint32_t b = (uint32_t)(row / lv.m), i = (uint32_t)(row % lv.m);
+            const uint32_t len = lv.pr.length(b);
+            const uint64_t i0 = (uint64_t)i * lv.L;
+            const uint64_t v = len > i0 ? umin64(len - i0, lv.L) : 0;
+            uint64_t sum = 0;
+            for (uint32_t j = 0; j < lv.s; ++j) sum += lv.a[q + j];
+            if (sum != v && atomicOr(flag, 2u) == 0) {
+                flag[1] = b; flag[2] = i; flag[3] = (unsigned)sum; flag[4] = (unsigned)v; flag[5] = len;
+                const u64 g = lv.samples[(uint64_t)b * ms + ms - 1];
+                flag[6] = (unsigned)(g >> 32); flag[7] = (unsigned)g;
+            }
         }
     }
-    if (v <= 0) return;
-    const uint64_t off = lv.pr.offset(b) + start;
-    (void)sm;
-    (void)vsm;
-    seg_sort_adaptive<KIND, BLOCK, ITEMS, GBS_ADAPT_DEPTH>(src, src_v, off, v, lv.out, lv.out_v, smem_raw);
 }
 
 // Nested Step 9: the buckets of this level become the problems of the next level.

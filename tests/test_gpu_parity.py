@@ -187,3 +187,42 @@ def test_dist_single_rank_nccl(dev):
     torch.cuda.synchronize()
     assert np.array_equal(to_np(out), np.sort(keys))
     assert L.gbs_comm_destroy(h) == 0
+
+
+def test_C4_pairs_full_size(dev):
+    """C4: 2^30 u32 -> u32 pairs (nested Step 9) in the bench's launch configuration.
+    Too large for the oracle; checked by properties that define a stable sort:
+    keys nondecreasing, values a permutation, keys_out == keys_in[values_out]
+    (values are input positions), equal keys keep increasing values."""
+    n = 1 << 30
+    keys_in = gi.generate_torch("uniform", n, seed=0, device=dev)
+    keys = keys_in.clone()
+    vals = torch.arange(n, dtype=torch.int32, device=dev)
+    assert len(gbs.plan(n, pairs=True)["levels"]) == 2
+    gbs.sort_pairs(keys, vals)
+    torch.cuda.synchronize()
+    k64 = keys.to(torch.int64) & 0xFFFFFFFF
+    assert bool((k64[1:] >= k64[:-1]).all())
+    seen = torch.zeros(n, dtype=torch.bool, device=dev)
+    seen[vals.long()] = True
+    assert bool(seen.all())
+    del seen
+    assert torch.equal(keys_in[vals.long()], keys)
+    eq = k64[1:] == k64[:-1]
+    assert bool((vals[1:][eq] > vals[:-1][eq]).all())
+
+
+@pytest.mark.parametrize("args", [("67108864", "32768", "64"), ("16777216", "32768", "512"),
+                                  ("33554432", "16384", "128")])
+def test_nested_invariants_debug_mode(dev, args):
+    """Nested Step 9 with many empty trailing sublists per problem (capacity = bound,
+    actual buckets ~half), run with GBS_DEBUG_SYNC=1: every launch synchronised and the
+    invariants of Steps 4 (sorted samples) and 6 (sum of a row = real items)
+    checked on device at every level; output == the plain definition."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "scripts", "debug_nested.py"), *args],
+                       capture_output=True, text=True, env=dict(os.environ, GBS_DEBUG_SYNC="1"), timeout=600)
+    assert "ok equal: True" in r.stdout, r.stdout + r.stderr

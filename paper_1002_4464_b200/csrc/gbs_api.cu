@@ -246,8 +246,8 @@ static void launch_seg_t(const LevelDev& lv, unsigned count, cudaStream_t st)
                                                           sm) != cudaSuccess || occ < 1)
             occ = 1;
     });
-    const unsigned grid = std::min<unsigned>(count, num_sms() * (unsigned)occ);
-    k_segment_sort<KIND, BLOCK, ITEMS, MODE><<<grid, BLOCK, sm, st>>>(lv);
+    (void)occ;
+    k_segment_sort<KIND, BLOCK, ITEMS, MODE><<<count, BLOCK, sm, st>>>(lv);   // one CTA per segment
 }
 
 // big / small CTA configurations per kind

@@ -96,7 +96,7 @@ __global__ void k_dist_cuts(const uint32_t* keys, size_t n_local, uint64_t gbase
     } while (0)
 
 struct DistLayout {
-    size_t sort_ws, samples, gathered, cuts, all_cuts, total;
+    size_t sort_ws, samples, gathered, cuts, all_cuts, u64ws, u64ws_bytes, total;
 };
 
 gbs_status_t dist_layout(size_t n_local, int p, DistLayout* L)
@@ -113,6 +113,11 @@ gbs_status_t dist_layout(size_t n_local, int p, DistLayout* L)
     L->gathered = o; o += al((size_t)p * s_r * 8);
     L->cuts = o;     o += al((size_t)p * 8);
     L->all_cuts = o; o += al((size_t)p * p * 8);
+    size_t u = 0;
+    r = gbs::sort_u64_ws((size_t)p * s_r, &u);
+    if (r) return r;
+    L->u64ws = o;    o += al(u);
+    L->u64ws_bytes = u;
     L->total = o;
     return GBS_SUCCESS;
 }
@@ -234,7 +239,7 @@ gbs_status_t gbs_sort_keys_dist(gbs_comm_t comm, uint32_t* d_keys, size_t n_loca
     k_dist_samples<<<(s_r + 255) / 256, 256, 0, st>>>(d_keys, n_local, s_r, gbase, samples);  // E2
     CUDA_OK(cudaGetLastError());
     NCCL_OK(ncclAllGather(samples, gathered, s_r, ncclUint64, comm->nc, st));            // E3
-    r = gbs::sort_u64_inplace(gathered, (size_t)p * s_r, nullptr, 0, st);               // E4
+    r = gbs::sort_u64_inplace(gathered, (size_t)p * s_r, w + L.u64ws, L.u64ws_bytes, st);  // E4
     if (r) return r;
     k_dist_cuts<<<(p + 127) / 128, 128, 0, st>>>(d_keys, n_local, gbase, gathered, s_r, p, cuts);  // E5-E6
     CUDA_OK(cudaGetLastError());

@@ -79,6 +79,7 @@ constexpr uint32_t TILE_KEYS = 1u << 15;   // u32 keys per CTA tile
 constexpr uint32_t TILE_PAIRS = 1u << 14;  // pairs per CTA tile (u64 on chip + values)
 constexpr uint32_t TILE_U64 = 1u << 14;    // u64 composites per CTA tile
 constexpr uint32_t SMALL_TILE = 2048;      // small CTA configuration
+constexpr uint64_t SMALL_U64_TOTAL = 1u << 18;   // u64 levels up to this many samples use 2K tiles
 constexpr uint32_t D_MIN = 8;              // single level needs d >= 8
 constexpr uint32_t D_NEST = 32;            // d of a level with a nested Step 9
 constexpr uint32_t MAX_S = 4096;           // shared-memory limit of Steps 6 and 8
@@ -145,10 +146,21 @@ static int build_node(Plan& P, int kind, uint32_t B, uint64_t N, uint32_t pad_ba
         L = cfg->L;
         s = cfg->s;
     } else {
-        L = tile;
-        for (uint32_t c = 2; c <= L / D_MIN; c *= 2)
-            if (hi_bound(N, L, c) <= tile) { s = c; break; }
-        if (!s) s = L / D_NEST;
+        // A small u64 level (few hundred thousand samples at most) would run as a handful
+        // of big-tile CTAs, i.e. at the latency of one CTA sort; with 2K tiles it spreads
+        // over many SMs.  Only when a single level with d >= D_MIN exists at that tile.
+        if (kind == KIND_U64 && (uint64_t)B * N <= SMALL_U64_TOTAL) {
+            for (uint32_t c = 2; c <= SMALL_TILE / D_MIN; c *= 2)
+                if (hi_bound(N, SMALL_TILE, c) <= SMALL_TILE) { s = c; break; }
+        }
+        if (s) {
+            L = SMALL_TILE;
+        } else {
+            L = tile;
+            for (uint32_t c = 2; c <= L / D_MIN; c *= 2)
+                if (hi_bound(N, L, c) <= tile) { s = c; break; }
+            if (!s) s = L / D_NEST;
+        }
     }
     nd.L = L;
     nd.s = s;

@@ -222,6 +222,9 @@ static gbs_status_t make_plan(size_t n, int kind, const gbs_config_t* cfg, Plan&
 
 // ----------------------------------------------------------------- launches
 static uint32_t num_sms();
+#ifndef GBS_IDX_TMA
+#define GBS_IDX_TMA 1
+#endif
 
 template <typename K>
 static void set_smem(K kernel, size_t bytes)
@@ -297,6 +300,18 @@ static void launch_seg(const LevelDev& lv, bool small, unsigned grid, cudaStream
 template <int KIND>
 static void launch_index(const LevelDev& lv, cudaStream_t st)
 {
+    const size_t kb = key_bytes(KIND);
+    // streaming TMA form when every chunk start is 16-byte aligned (contiguous problems)
+    const bool tma = GBS_IDX_TMA && lv.pr.off == nullptr && ((uintptr_t)lv.in & 15) == 0 &&
+                     (lv.pr.stride * kb) % 16 == 0 && ((size_t)lv.L * kb) % 16 == 0 && lv.s <= 8 * IDX_BLOCK;
+    if (tma) {
+        const size_t sm = 2 * (size_t)IDX_CHUNK_BYTES + (size_t)lv.s * 12;
+        static std::once_flag f2;
+        std::call_once(f2, [&] { set_smem(k_sample_index_tma<KIND, IDX_BLOCK, 8>, 220 * 1024); });
+        const unsigned grid = std::min<unsigned>(lv.B * lv.m, num_sms());
+        k_sample_index_tma<KIND, IDX_BLOCK, 8><<<grid, IDX_BLOCK, sm, st>>>(lv);
+        return;
+    }
     const size_t chunk = std::min<size_t>((size_t)lv.L * key_bytes(KIND), IDX_CHUNK_BYTES);
     const size_t sm = (size_t)lv.s * 8 + (size_t)(lv.s + (lv.s & 1)) * 4 + chunk;
     static std::once_flag f;

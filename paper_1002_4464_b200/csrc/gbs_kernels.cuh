@@ -344,6 +344,165 @@ __global__ void k_global_samples(LevelDev lv)
 // GT200 bank contention and does not change the result (R10).
 static constexpr int IDX_CHUNK_BYTES = 64 * 1024;
 
+// --- TMA bulk copy + mbarrier helpers (sm_90+ PTX; SASS UBLKCP / SYNCS)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, unsigned bytes, unsigned long long* bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase)
+{
+    asm volatile("{\n\t.reg .pred p;\n\tLAB_WAIT:\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                 "@!p bra LAB_WAIT;\n\t}" ::"r"(smem_u32(bar)), "r"(phase) : "memory");
+}
+
+// Step 6, streaming form: persistent CTAs walk (sublist, 64 KB chunk) work items; one
+// thread keeps the next chunk's TMA bulk copy in flight (double buffer) while all
+// threads bisect the current one.  Used when every chunk start is 16-byte aligned
+// (contiguous problems; the host checks); per-splitter counts accumulate in registers.
+template <int KIND, int BLOCK, int MAXQ>
+__global__ void __launch_bounds__(BLOCK, 1) k_sample_index_tma(LevelDev lv)
+{
+    using KT = typename std::conditional<KIND == KIND_U64, unsigned long long, uint32_t>::type;
+    constexpr int CH = IDX_CHUNK_BYTES / sizeof(KT);
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    KT* buf0 = reinterpret_cast<KT*>(smem_raw);
+    KT* buf1 = buf0 + CH;
+    unsigned long long* gs = reinterpret_cast<unsigned long long*>(buf1 + CH);
+    uint32_t* Q = reinterpret_cast<uint32_t*>(gs + lv.s);
+    __shared__ __align__(8) unsigned long long bars[2];
+
+    const uint32_t ntiles = lv.B * lv.m;
+    // chunks of tile t: ceil(v / CH); work items in order (tile, chunk)
+    auto tile_v = [&](uint32_t t) -> int {
+        const uint32_t b = t / lv.m, i = t % lv.m;
+        const uint32_t len = lv.pr.length(b);
+        const uint64_t i0 = (uint64_t)i * lv.L;
+        return len > i0 ? (int)umin64(len - i0, lv.L) : 0;
+    };
+    auto issue = [&](uint32_t t, int c, int slot) {   // thread 0 only
+        const int v = tile_v(t);
+        const int cl = min(CH, v - c * CH);
+        const unsigned bytes = (unsigned)((size_t)cl * sizeof(KT)) & ~15u;
+        const KT* src = reinterpret_cast<const KT*>(lv.in) + lv.pr.offset(t / lv.m) + (uint64_t)(t % lv.m) * lv.L +
+                        (uint64_t)c * CH;
+        unsigned long long* bar = &bars[slot];
+        mbar_expect_tx(bar, bytes);
+        if (bytes) tma_load_1d(slot ? buf1 : buf0, src, bytes, bar);
+    };
+    if (threadIdx.x == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    uint32_t tile = blockIdx.x;
+    // first work item: skip empty tiles
+    while (tile < ntiles && tile_v(tile) == 0) {
+        // an empty sublist still owns a row of zeros
+        uint32_t* arow = lv.a + (uint64_t)tile * lv.s;
+        for (uint32_t j = threadIdx.x; j < lv.s; j += BLOCK) arow[j] = 0;
+        tile += gridDim.x;
+    }
+    if (tile >= ntiles) return;
+    int chunk = 0;
+    if (threadIdx.x == 0) issue(tile, 0, 0);
+    uint32_t loaded_b = 0xFFFFFFFFu;
+    uint32_t q[MAXQ];
+#pragma unroll
+    for (int k = 0; k < MAXQ; ++k) q[k] = 0;
+    unsigned phase = 0;   // bit k: parity of the next completion of bars[k]
+    int slot = 0;
+    while (true) {
+        const uint32_t b = tile / lv.m, i = tile % lv.m;
+        const int v = tile_v(tile);
+        const int nch = (v + CH - 1) / CH;
+        const uint64_t i0 = (uint64_t)i * lv.L;
+        // next work item (same tile's next chunk, else the next non-empty tile)
+        uint32_t ntile = tile;
+        int nchunk = chunk + 1;
+        if (nchunk >= nch) {
+            nchunk = 0;
+            ntile = tile + gridDim.x;
+            while (ntile < ntiles && tile_v(ntile) == 0) ntile += gridDim.x;   // rows zeroed below
+        }
+        if (threadIdx.x == 0 && ntile < ntiles) issue(ntile, nchunk, slot ^ 1);
+        if (b != loaded_b) {          // splitters of problem b (Step 5 fused)
+            const u64* srt = lv.samples + (uint64_t)b * lv.m * lv.s;
+            for (uint32_t j = threadIdx.x; j < lv.s; j += BLOCK) {
+                const u64 gj = srt[(uint64_t)(j + 1) * lv.m - 1];
+                gs[j] = gj;
+                if (i == 0) lv.splitters[(uint64_t)b * lv.s + j] = gj;
+            }
+            loaded_b = b;
+        }
+        KT* ks = slot ? buf1 : buf0;
+        mbar_wait(&bars[slot], (phase >> slot) & 1u);
+        phase ^= 1u << slot;
+        const int c0 = chunk * CH;
+        const int cl = min(CH, v - c0);
+        {   // keys past the last 16-byte boundary of the chunk (tail of the sublist)
+            const int full = (int)(((unsigned)((size_t)cl * sizeof(KT)) & ~15u) / sizeof(KT));
+            const KT* src = reinterpret_cast<const KT*>(lv.in) + lv.pr.offset(b) + i0 + c0;
+            for (int p = full + threadIdx.x; p < cl; p += BLOCK) ks[p] = src[p];
+        }
+        __syncthreads();
+        auto rank_key = [&](int p) -> unsigned long long {
+            if (KIND == KIND_U64) return (unsigned long long)ks[p];
+            return ((unsigned long long)ks[p] << 32) | (uint32_t)(i0 + c0 + p);
+        };
+        const unsigned long long first = rank_key(0), last = rank_key(cl - 1);
+#pragma unroll
+        for (int k = 0; k < MAXQ; ++k) {
+            const uint32_t j = threadIdx.x + k * BLOCK;
+            if (j < lv.s) {
+                const unsigned long long gj = gs[j];
+                int lo = 0, hi = cl;
+                if (gj < first) hi = 0;
+                else if (gj >= last) lo = cl;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (rank_key(mid) <= gj) lo = mid + 1; else hi = mid;
+                }
+                q[k] += (uint32_t)lo;
+            }
+        }
+        if (chunk + 1 >= nch) {       // sublist done: a_ij = Q_ij - Q_i,j-1
+#pragma unroll
+            for (int k = 0; k < MAXQ; ++k) {
+                const uint32_t j = threadIdx.x + k * BLOCK;
+                if (j < lv.s) Q[j] = q[k];
+                q[k] = 0;
+            }
+            __syncthreads();
+            uint32_t* arow = lv.a + ((uint64_t)b * lv.m + i) * lv.s;
+            for (uint32_t j = threadIdx.x; j < lv.s; j += BLOCK) arow[j] = Q[j] - (j ? Q[j - 1] : 0u);
+            // empty sublists skipped on the way to the next tile get rows of zeros
+            for (uint32_t t2 = tile + gridDim.x; t2 < ntile && t2 < ntiles; t2 += gridDim.x) {
+                uint32_t* zrow = lv.a + (uint64_t)t2 * lv.s;
+                for (uint32_t j = threadIdx.x; j < lv.s; j += BLOCK) zrow[j] = 0;
+            }
+        }
+        __syncthreads();              // buffer `slot` free; Q / gs reusable
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (ntile >= ntiles) break;
+        tile = ntile;
+        chunk = nchunk;
+        slot ^= 1;
+    }
+}
+
 template <int KIND, int BLOCK>
 __global__ void __launch_bounds__(BLOCK, 2) k_sample_index(LevelDev lv)
 {

@@ -735,6 +735,15 @@ __global__ void __launch_bounds__(BLOCK, 2) k_relocate(LevelDev lv)
         if (KIND == KIND_PAIRS) prefetch_l2(lv.in_v + ps, (size_t)pv * 4);
     }
 
+    // the first batch of keys is loaded now; its latency overlaps the map build
+    constexpr int U = 8;
+    KT y[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int r = threadIdx.x + u * BLOCK;
+        y[u] = r < v ? src[r] : KT(0);
+    }
+
     const uint64_t row = ((uint64_t)b * lv.m + i) * lv.s;
     for (uint32_t j = threadIdx.x; j < lv.s; j += BLOCK) starts[j] = lv.a[row + j];
     __syncthreads();
@@ -761,28 +770,45 @@ __global__ void __launch_bounds__(BLOCK, 2) k_relocate(LevelDev lv)
         }
     }
     __syncthreads();
+    // position-ordered copy, software-pipelined: batch k+1 is loaded before batch k is
+    // stored, so one batch of loads is always in flight (the compiler cannot reorder the
+    // loads above the stores itself: src and dst may alias as far as it knows)
     KT* dst = reinterpret_cast<KT*>(lv.reloc) + off;
-    for (int q0 = threadIdx.x; q0 < v; q0 += 8 * BLOCK) {
-        KT y[8];
+    for (int q0 = threadIdx.x; q0 < v; q0 += U * BLOCK) {
+        KT z[U];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) y[u] = q0 + u * BLOCK < v ? src[q0 + u * BLOCK] : KT(0);
+        for (int u = 0; u < U; ++u) {
+            const int r = q0 + (U + u) * BLOCK;
+            z[u] = r < v ? src[r] : KT(0);
+        }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < U; ++u) {
             const int r = q0 + u * BLOCK;
             if (r < v) dst[(uint32_t)r + delta[bmap[r + 2 * (r >> lp)]]] = y[u];
+            y[u] = z[u];
         }
     }
     if (KIND == KIND_PAIRS) {
         const uint32_t* sv = lv.in_v + off + i0;
         uint32_t* dv = lv.reloc_v + off;
-        for (int q0 = threadIdx.x; q0 < v; q0 += 8 * BLOCK) {
-            uint32_t y[8];
+        uint32_t w[U];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) y[u] = q0 + u * BLOCK < v ? sv[q0 + u * BLOCK] : 0u;
+        for (int u = 0; u < U; ++u) {
+            const int r = threadIdx.x + u * BLOCK;
+            w[u] = r < v ? sv[r] : 0u;
+        }
+        for (int q0 = threadIdx.x; q0 < v; q0 += U * BLOCK) {
+            uint32_t z[U];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < U; ++u) {
+                const int r = q0 + (U + u) * BLOCK;
+                z[u] = r < v ? sv[r] : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
                 const int r = q0 + u * BLOCK;
-                if (r < v) dv[(uint32_t)r + delta[bmap[r + 2 * (r >> lp)]]] = y[u];
+                if (r < v) dv[(uint32_t)r + delta[bmap[r + 2 * (r >> lp)]]] = w[u];
+                w[u] = z[u];
             }
         }
     }

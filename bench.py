@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--dist", default="uniform")
     ap.add_argument("--impl", default="gbs", choices=["gbs", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="use the multi-GPU entry even with one rank (exercises E1-E9 on one GPU)")
     return ap.parse_args()
 
 
@@ -222,11 +224,14 @@ def main():
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    use_dist = world > 1 or args.force_dist
+    if use_dist:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29531")
+        dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
     if rank == 0:
         _build.build()
-    if world > 1:
+    if use_dist:
         dist.barrier()
 
     n, wl = WORKLOADS[args.workload]
@@ -237,14 +242,14 @@ def main():
     else:
         pristine = gi.generate_torch(args.dist, n * world, seed=0, device=dev, start=n * rank, count=n)
     pairs = args.workload == "C4"
-    if pairs and world > 1:
+    if pairs and use_dist:
         raise SystemExit("the multi-GPU entry sorts keys (DESIGN.md 7); C4 is a single-GPU workload")
     keys = torch.empty_like(pristine)
     vals = torch.empty_like(pristine) if pairs else None
     pristine_v = torch.arange(n, dtype=torch.int32, device=dev) if pairs else None
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
     ws = gbs.Workspace(dev)
-    comm = gbs.Comm() if world > 1 else None
+    comm = gbs.Comm() if use_dist else None
     out = None
     if comm is not None:
         _, cap = gbs.dist_workspace_size(n, world)
@@ -283,10 +288,25 @@ def main():
             ref = torch.sort(pristine.to(torch.int64) & 0xFFFFFFFF).values
             assert torch.equal(keys.to(torch.int64) & 0xFFFFFFFF, ref), "sort mismatch"
             del ref
+    else:   # multi-GPU: every rank's part sorted, parts ordered across ranks, nothing lost
+        restore()
+        part = gbs.sort_keys_dist(keys, comm, out=out, ws=ws)
+        p64 = part.to(torch.int64) & 0xFFFFFFFF
+        ok = bool((p64[1:] >= p64[:-1]).all()) if part.numel() > 1 else True
+        info = torch.tensor([part.numel(), int(p64[0]) if part.numel() else -1,
+                             int(p64[-1]) if part.numel() else -1, int(ok)], dtype=torch.int64, device=dev)
+        allinfo = [torch.empty_like(info) for _ in range(world)]
+        dist.all_gather(allinfo, info)
+        rows = [t.tolist() for t in allinfo]
+        assert sum(r[0] for r in rows) == n * world, "multi-GPU sort lost keys"
+        assert all(r[3] for r in rows), "a rank's part is not sorted"
+        ends = [(r[1], r[2]) for r in rows if r[0] > 0]
+        assert all(ends[k][1] <= ends[k + 1][0] for k in range(len(ends) - 1)), "parts out of order"
+        del p64
 
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    if world > 1:
+    if use_dist:
         dist.barrier()
     torch.cuda.synchronize()
     if comm is None:
@@ -300,11 +320,11 @@ def main():
             ends[i].record(stream)
         torch.cuda.synchronize()
     prof = gbs.profile_end() if comm is None else None
-    if world > 1:
+    if use_dist:
         dist.barrier()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     ms = statistics.mean(step_ms)
-    if world > 1:
+    if use_dist:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
@@ -333,12 +353,41 @@ def main():
         em = statistics.mean(e_ms)
         e2e = {"value": n / (em / 1e3), "unit": "keys/s", "h2d_bytes_per_step": 4 * n,
                "d2h_bytes_per_step": 4 * n, "ms_per_step": em}
+    elif comm is not None:
+        # end to end per rank: pinned host shard -> device, multi-GPU sort, the rank's
+        # part back to pinned host; max over ranks
+        host = pristine.cpu().pin_memory()
+        hout = torch.empty(out.numel(), dtype=torch.int32).pin_memory()
+        e_ms, moved = [], 0
+        for i in range(max(3, args.steps // 2) + 1):
+            dist.barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            keys.copy_(host, non_blocking=True)
+            part = gbs.sort_keys_dist(keys, comm, out=out, ws=ws)
+            hout[:part.numel()].copy_(part, non_blocking=True)
+            b.record(stream)
+            b.synchronize()
+            if i:                                            # first iteration = warm-up
+                e_ms.append(a.elapsed_time(b))
+            moved = part.numel()
+        t = torch.tensor([statistics.mean(e_ms), moved], dtype=torch.float64, device=dev)
+        tmax = t.clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        em = float(tmax[0].item())
+        e2e = {"value": n * world / (em / 1e3), "unit": "keys/s", "h2d_bytes_per_step": 4 * n * world,
+               "d2h_bytes_per_step": 4 * n * world, "ms_per_step": em}
 
     if rank != 0:
-        if world > 1:
+        if use_dist:
             dist.destroy_process_group()
         return
 
+    # our kernels per step: the plan's launches; multi-GPU adds E2 + E5/E6 + the E4
+    # single-tile sample sort and the E9 re-sort of the received runs (~ n keys)
+    launches_per_step = plan["kernels_per_sort"]
+    if comm is not None:
+        launches_per_step += 3 + gbs.plan(n)["kernels_per_sort"]
     peak, peak_src = peaks()
     roof = None
     steps = None
@@ -370,11 +419,11 @@ def main():
                        "plan": plan["levels"], "bucket_bound": plan["bucket_bound"],
                        "l2": "flushed between steps (256 MiB memset) outside the event window",
                        "parallelism": f"dp{world}" if world > 1 else "single"},
-            "e2e": e2e, "gpu_launches": plan["kernels_per_sort"] * args.steps,
+            "e2e": e2e, "gpu_launches": launches_per_step * args.steps,
             "clocks": clk.summary(), "roofline": roof, "cpu_baseline": cpu, "steps_breakdown": steps,
             "step_ms_min_max": [min(step_ms), max(step_ms)]}
     print(json.dumps(line))
-    if world > 1:
+    if use_dist:
         comm.close()
         dist.destroy_process_group()
 

@@ -134,7 +134,7 @@ const char* gbs_last_error(void); /* thread-local */
  * s_r regular samples (E2), allgathers them (E3, NCCL), sorts them and picks p
  * splitters identically on every rank (E4-E5), cuts its sorted shard (E6),
  * allgathers the p x p counts (E7), exchanges buckets with grouped send/recv over
- * NVLink (E8) and sorts what it received (E9). */
+ * NVLink (E8) and merges the p sorted runs it received (E9, gbs_merge_runs). */
 typedef struct gbs_comm* gbs_comm_t;
 #define GBS_UNIQUE_ID_BYTES 128 /* == sizeof(ncclUniqueId) */
 
@@ -165,6 +165,15 @@ gbs_status_t gbs_sort_keys_dist(gbs_comm_t comm, uint32_t* d_keys, size_t n_loca
 gbs_status_t gbs_exchange_plan(const uint64_t* cuts, int p, int rank, uint64_t* send_off,
                                uint64_t* send_cnt, uint64_t* recv_off, uint64_t* recv_cnt,
                                uint64_t* n_out);
+
+/* Merge p sorted runs of u32 keys (E9 of the multi-GPU level: the runs a rank receives,
+ * one per source rank, each sorted).  d_keys[run_off[r] .. run_off[r+1]) is run r
+ * (run_off: host array of p+1 offsets, run_off[0] = 0, nondecreasing, run_off[p] = n);
+ * on return d_keys[0..n) is sorted (in place; ties keep run order).  A pairwise merge-path
+ * tree: ceil(log2 p) passes through the workspace.  p <= 64. */
+gbs_status_t gbs_merge_runs_workspace_size(size_t n, int p, size_t* bytes);
+gbs_status_t gbs_merge_runs(uint32_t* d_keys, const uint64_t* run_off, int p, void* d_ws, size_t ws_bytes,
+                            gbs_stream_t stream);
 
 #ifdef __cplusplus
 }

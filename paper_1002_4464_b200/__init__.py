@@ -77,6 +77,8 @@ def lib():
             "gbs_exchange_plan": [p, C.c_int, C.c_int, p, p, p, p, p],
             "gbs_profile_begin": [],
             "gbs_profile_end": [C.POINTER(StepTimes)],
+            "gbs_merge_runs_workspace_size": [sz, C.c_int, C.POINTER(sz)],
+            "gbs_merge_runs": [p, p, C.c_int, p, sz, p],
         }
         for name, args in sigs.items():
             f = getattr(L, name)
@@ -241,6 +243,19 @@ def sort_keys_host(h_keys, d_buf, ws: Workspace | None = None, stream=None):
     _check(lib().gbs_sort_keys_host(C.c_void_p(h_keys.data_ptr()), n, C.c_void_p(dp), wp, wb,
                                     _stream(stream)))
     return h_keys
+
+
+def merge_runs(keys, run_off, ws: Workspace | None = None, stream=None):
+    """Merge sorted runs keys[run_off[r]:run_off[r+1]] in place (E9 of the multi-GPU level)."""
+    import numpy as np
+    off = np.ascontiguousarray(run_off, dtype=np.uint64)
+    p = off.size - 1
+    kp = _dev_ptr(keys, "keys")
+    need = C.c_size_t()
+    _check(lib().gbs_merge_runs_workspace_size(int(off[-1]), p, C.byref(need)))
+    wp, wb = _ws_for(need.value, ws, keys.device)
+    _check(lib().gbs_merge_runs(C.c_void_p(kp), off.ctypes.data_as(C.c_void_p), p, wp, wb, _stream(stream)))
+    return keys
 
 
 # ----------------------------------------------------------------- multi GPU

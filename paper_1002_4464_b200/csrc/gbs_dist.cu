@@ -11,7 +11,7 @@
 //   E6 cut points by bisection in the sorted shard                        (Step 6)
 //   E7 allgather of the p x p cut matrix, one D2H + stream sync           (Step 7)
 //   E8 grouped ncclSend/ncclRecv over NVLink: contiguous runs, no pack    (Step 8)
-//   E9 sort of the received runs with the single-GPU path                 (Step 9)
+//   E9 p-way merge of the received runs (gbs_merge_runs, gbs_merge.cu)   (Step 9)
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -104,7 +104,7 @@ gbs_status_t dist_layout(size_t n_local, int p, DistLayout* L)
     size_t a = 0, b = 0;
     gbs_status_t r = gbs_sort_keys_workspace_size(n_local, &a);
     if (r) return r;
-    r = gbs_sort_keys_workspace_size(out_cap(n_local, p), &b);
+    r = gbs_merge_runs_workspace_size(out_cap(n_local, p), p, &b);     // E9 (p-way merge)
     if (r) return r;
     const uint32_t s_r = s_r_of(n_local);
     L->sort_ws = 0;
@@ -261,7 +261,12 @@ gbs_status_t gbs_sort_keys_dist(gbs_comm_t comm, uint32_t* d_keys, size_t n_loca
     NCCL_OK(ncclGroupEnd());
     if (sc[rank])
         CUDA_OK(cudaMemcpyAsync(d_out + ro[rank], d_keys + so[rank], sc[rank] * 4, cudaMemcpyDeviceToDevice, st));
-    r = gbs_sort_keys(d_out, total, w, sort_ws, stream);                                 // E9
+    {   // E9: the p received runs (one per source rank, each sorted) -> one sorted run
+        std::vector<uint64_t> roff(p + 1);
+        for (int k = 0; k < p; ++k) roff[k] = ro[k];
+        roff[p] = total;
+        r = gbs_merge_runs(d_out, roff.data(), p, w, sort_ws, stream);
+    }
     if (r) return r;
     *n_out = total;
     return GBS_SUCCESS;

@@ -375,7 +375,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_sample_index_tma(LevelDev lv)
 {
     using KT = typename std::conditional<KIND == KIND_U64, unsigned long long, uint32_t>::type;
     constexpr int CH = IDX_CHUNK_BYTES / sizeof(KT);
-    extern __shared__ __align__(128) unsigned char smem_raw[];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
     KT* buf0 = reinterpret_cast<KT*>(smem_raw);
     KT* buf1 = buf0 + CH;
     unsigned long long* gs = reinterpret_cast<unsigned long long*>(buf1 + CH);

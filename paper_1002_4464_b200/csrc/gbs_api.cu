@@ -79,6 +79,10 @@ constexpr uint32_t TILE_KEYS = 1u << 15;   // u32 keys per CTA tile
 constexpr uint32_t TILE_PAIRS = 1u << 14;  // pairs per CTA tile (u64 on chip + values)
 constexpr uint32_t TILE_U64 = 1u << 14;    // u64 composites per CTA tile
 constexpr uint32_t SMALL_TILE = 2048;      // small CTA configuration
+#ifndef GBS_SPLIT_STEP9
+#define GBS_SPLIT_STEP9 1
+#endif
+constexpr bool GBS_SPLIT_STEP9_ON = GBS_SPLIT_STEP9;
 constexpr uint64_t SMALL_U64_TOTAL = 1u << 18;   // u64 levels up to this many samples use 2K tiles
 constexpr uint32_t D_MIN = 8;              // single level needs d >= 8
 constexpr uint32_t D_NEST = 32;            // d of a level with a nested Step 9
@@ -108,6 +112,13 @@ struct Node {
     size_t o_samples = 0, o_splitters = 0, o_a = 0, o_l = 0, o_state = 0;
     size_t o_child_off = 0, o_child_len = 0, o_reloc = SIZE_MAX, o_reloc_v = SIZE_MAX;
 };
+
+// Step 9 in two launches (<= half a tile on 512-thread CTAs, the rest on 1024) when the
+// buckets use the big configuration and may exceed half a tile.
+static bool split_step9(int kind, const Node& nd)
+{
+    return !nd.bucket_small && nd.step9 < 0 && nd.hi > tile_of(kind) / 2;
+}
 
 struct Plan {
     std::vector<Node> nodes;
@@ -190,7 +201,8 @@ static int build_node(Plan& P, int kind, uint32_t B, uint64_t N, uint32_t pad_ba
     P.nodes[idx].step4 = c4;
     if (nd.hi <= tile) {
         P.nodes[idx].bucket_small = nd.hi <= SMALL_TILE;
-        P.launches += 1;
+        // buckets that may exceed half a tile: two Step-9 launches (see exec_kind)
+        P.launches += (GBS_SPLIT_STEP9_ON && split_step9(kind, P.nodes[idx])) ? 2 : 1;
     } else {
         P.nodes[idx].o_child_off = P.alloc((uint64_t)B * s * 8);
         P.nodes[idx].o_child_len = P.alloc((uint64_t)B * s * 4);
@@ -222,6 +234,9 @@ static gbs_status_t make_plan(size_t n, int kind, const gbs_config_t* cfg, Plan&
 
 // ----------------------------------------------------------------- launches
 static uint32_t num_sms();
+#ifndef GBS_SPLIT_STEP9
+#define GBS_SPLIT_STEP9 1
+#endif
 #ifndef GBS_IDX_TMA
 #define GBS_IDX_TMA 1
 #endif
@@ -376,6 +391,8 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
     lv.out_v = bf.out_v;
     lv.pf_stride = num_sms();
     lv.presorted = pr.presorted;
+    lv.seg_min = 0;
+    lv.seg_max = 0xFFFFFFFFu;
     if (nd.leaf) {
         launch_seg<KIND, MODE_LEAF>(lv, nd.small, nd.B, st);
         GBS_LAUNCHED();
@@ -465,7 +482,22 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
 
     // Step 9: bucket sort reloc -> out (one CTA per bucket) or a nested level
     if (nd.step9 < 0) {
-        launch_seg<KIND, MODE_BUCKET>(lv, nd.bucket_small, nd.B * nd.s, st);
+        constexpr uint32_t TILE = tile_of_c(KIND);
+        constexpr int ITEMS = KIND == KIND_KEYS ? GBS_KEYS_ITEMS : GBS_WIDE_ITEMS;
+        if (GBS_SPLIT_STEP9_ON && split_step9(KIND, nd)) {
+            // buckets of at most half a tile go to a 512-thread CTA (2 per SM: one's
+            // load/store phases overlap the other's sort); larger ones to 1024 threads
+            LevelDev lo = lv, hi = lv;
+            lo.seg_max = TILE / 2;
+            hi.seg_min = TILE / 2;
+            launch_seg_t<KIND, 512, ITEMS, MODE_BUCKET>(lo, nd.B * nd.s, st);
+            GBS_LAUNCHED();
+            if constexpr (KIND == KIND_KEYS) launch_seg_t<KIND, GBS_BIG_KEYS, MODE_BUCKET>(hi, nd.B * nd.s, st);
+            else launch_seg_t<KIND, GBS_BIG_WIDE, MODE_BUCKET>(hi, nd.B * nd.s, st);
+            GBS_LAUNCHED();
+        } else {
+            launch_seg<KIND, MODE_BUCKET>(lv, nd.bucket_small, nd.B * nd.s, st);
+        }
         GBS_LAUNCHED();
     } else {
         lv.child_off = reinterpret_cast<u64*>(ws + nd.o_child_off);

@@ -56,6 +56,7 @@ struct LevelDev {
     uint32_t* child_len;
     uint32_t pf_stride;    // co-resident CTAs (SMs x CTAs/SM): CTA b prefetches CTA b + pf_stride
     uint32_t presorted;    // input consists of sorted runs of this length (Step 4 levels), 0 = none
+    uint32_t seg_min, seg_max;   // k_segment_sort: this launch sorts segments of seg_min < v <= seg_max
 };
 
 // L2 prefetch of a byte range (cp.async.bulk.prefetch: a TMA bulk operation, no
@@ -842,7 +843,7 @@ __device__ __forceinline__ void segment_of(const LevelDev& lv, uint32_t idx, uin
 // walked segments with a work counter and register prefetch measured ~8% slower: the
 // shared register array across tile sizes costs more than the hidden load latency.)
 template <int KIND, int BLOCK, int ITEMS, int MODE>
-__global__ void __launch_bounds__(BLOCK, 1) k_segment_sort(LevelDev lv)
+__global__ void __launch_bounds__(BLOCK, (BLOCK <= 512 ? 2 : 1)) k_segment_sort(LevelDev lv)
 {
     using A = Adapt<KIND, BLOCK, ITEMS, GBS_ADAPT_DEPTH>;
     using KeyT = typename A::S::KeyT;
@@ -862,7 +863,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_segment_sort(LevelDev lv)
     uint64_t off;
     int v;
     segment_of<MODE>(lv, blockIdx.x, off, v);
-    if (v <= 0) return;
+    if (v <= 0 || (uint32_t)v <= lv.seg_min || (uint32_t)v > lv.seg_max) return;
     A::run(src, src_v, off, v, lv.out, lv.out_v, smem_raw);
 }
 

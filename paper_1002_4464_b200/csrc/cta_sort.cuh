@@ -20,6 +20,9 @@ namespace gbs {
 
 template <int X> struct Log2 { static constexpr int value = 1 + Log2<X / 2>::value; };
 template <> struct Log2<1> { static constexpr int value = 0; };
+// trailing zero bits: ITEMS = 2^Ctz * odd
+template <int X> struct Ctz { static constexpr int value = (X & 1) ? 0 : 1 + Ctz<X / 2>::value; };
+template <> struct Ctz<0> { static constexpr int value = 0; };
 
 template <typename T>
 __device__ __forceinline__ void cas(T& a, T& b)
@@ -93,10 +96,11 @@ __device__ __forceinline__ void reg_sort(T (&x)[M])
 template <typename T, int BLOCK, int ITEMS, int CHAINS_ = 0, int PAD_ = GBS_PAD_SHIFT>
 struct CtaSort {
     static constexpr int TILE = BLOCK * ITEMS;
-    static constexpr int LOG_ITEMS = Log2<ITEMS>::value;
+    static constexpr int LOG_ITEMS = Ctz<ITEMS>::value;   // log2(ITEMS) for a power of two
     static constexpr int WARP_SPAN = 32 * ITEMS;                  // items owned by one warp
-    // Shared-memory layout: one pad slot every 2^PAD items.  PAD = log2(ITEMS) makes the
-    // blocked stores conflict-free; a finer pad spreads the merge reads, whose lanes sit
+    // Shared-memory layout: one pad slot every 2^PAD items.  PAD = ctz(ITEMS) (log2 for a
+    // power of two) makes a thread's stride ITEMS + ITEMS/2^PAD odd, so the blocked
+    // stores are conflict-free; a finer pad spreads the merge reads, whose lanes sit
     // ~ITEMS/2 elements apart in each run.
     static constexpr int PAD = PAD_ > 0 ? PAD_ : LOG_ITEMS;
     static constexpr int SMEM_ELEMS = TILE + (TILE >> PAD) + 2;
@@ -143,7 +147,9 @@ struct CtaSort {
     {
         static_assert(M >= ITEMS, "register array too small");
         constexpr int H = ITEMS / CHAINS;
-        const int base = start & ~(2 * w - 1);
+        // w = ITEMS * 2^k; ITEMS itself need not be a power of two (the pair index is
+        // taken on the thread index start / ITEMS)
+        const int base = ((start / ITEMS) & ~(2 * (w / ITEMS) - 1)) * ITEMS;
         const int aEnd = base + w, bEnd = base + 2 * w;
         int ai[CHAINS], cb[CHAINS];
         T a[CHAINS], b[CHAINS];

@@ -111,13 +111,50 @@ struct Node {
     int step4 = -1, step9 = -1;
     size_t o_samples = 0, o_splitters = 0, o_a = 0, o_l = 0, o_state = 0;
     size_t o_child_off = 0, o_child_len = 0, o_reloc = SIZE_MAX, o_reloc_v = SIZE_MAX;
+    size_t o_tiers = 0;   // Step 9 size-tier lists (3 x B*s) + counters (4)
 };
 
-// Step 9 in two launches (<= half a tile on 512-thread CTAs, the rest on 1024) when the
-// buckets use the big configuration and may exceed half a tile.
+// big / small CTA configurations per kind
+// (overridable with -D for tuning experiments)
+#ifndef GBS_KEYS_BLOCK
+#define GBS_KEYS_BLOCK 1024
+#define GBS_KEYS_ITEMS 32
+#endif
+#ifndef GBS_WIDE_BLOCK
+#define GBS_WIDE_BLOCK 1024
+#define GBS_WIDE_ITEMS 16
+#endif
+#define GBS_BIG_KEYS GBS_KEYS_BLOCK, GBS_KEYS_ITEMS
+#define GBS_BIG_WIDE GBS_WIDE_BLOCK, GBS_WIDE_ITEMS
+#ifndef GBS_SMALL
+#define GBS_SMALL 256, 8
+#endif
+
+// Step 9 in size tiers (<= half a tile on 512-thread CTAs, then a 1024-thread mid tier,
+// then the full tile) when the buckets use the big configuration and may exceed half a
+// tile.
+#ifndef GBS_MID_STEP9
+#define GBS_MID_STEP9 1
+#endif
+// Step 9 mid tier: 5/8 of the full tile; keys on 512 threads x 40 (64 registers, 2 CTAs
+// per SM), 8-byte items on 1024 x 10 (20 u64 per thread would spill)
+#define MID_BLOCK_OF(KIND) ((KIND) == KIND_KEYS ? 512 : 1024)
+#define MID_ITEMS_OF(KIND) ((KIND) == KIND_KEYS ? GBS_KEYS_ITEMS * 5 / 4 : GBS_WIDE_ITEMS * 5 / 8)
+static constexpr uint32_t mid_cap(int kind)
+{
+    return kind == KIND_KEYS ? 512u * (GBS_KEYS_ITEMS * 5 / 4) : 1024u * (GBS_WIDE_ITEMS * 5 / 8);
+}
 static bool split_step9(int kind, const Node& nd)
 {
     return !nd.bucket_small && nd.step9 < 0 && nd.hi > tile_of(kind) / 2;
+}
+// Step 9 launches of a CTA-bucket node: one, or the size tiers <= tile/2, mid, > mid
+static int step9_launches(int kind, const Node& nd)
+{
+    if (!(GBS_SPLIT_STEP9_ON && split_step9(kind, nd))) return 1;
+    // + the classification kernel (k_bucket_tiers)
+    if (!GBS_MID_STEP9) return 3;
+    return nd.hi > mid_cap(kind) ? 4 : 3;
 }
 
 struct Plan {
@@ -201,8 +238,10 @@ static int build_node(Plan& P, int kind, uint32_t B, uint64_t N, uint32_t pad_ba
     P.nodes[idx].step4 = c4;
     if (nd.hi <= tile) {
         P.nodes[idx].bucket_small = nd.hi <= SMALL_TILE;
-        // buckets that may exceed half a tile: two Step-9 launches (see exec_kind)
-        P.launches += (GBS_SPLIT_STEP9_ON && split_step9(kind, P.nodes[idx])) ? 2 : 1;
+        // buckets that may exceed half a tile: size tiers (see exec_kind)
+        P.launches += step9_launches(kind, P.nodes[idx]);
+        if (GBS_SPLIT_STEP9_ON && split_step9(kind, P.nodes[idx]))
+            P.nodes[idx].o_tiers = P.alloc(((uint64_t)B * s * 3 + 4) * 4);
     } else {
         P.nodes[idx].o_child_off = P.alloc((uint64_t)B * s * 8);
         P.nodes[idx].o_child_len = P.alloc((uint64_t)B * s * 4);
@@ -277,24 +316,10 @@ static void launch_seg_t(const LevelDev& lv, unsigned count, cudaStream_t st)
             occ = 1;
     });
     (void)occ;
-    k_segment_sort<KIND, BLOCK, ITEMS, MODE><<<count, BLOCK, sm, st>>>(lv);   // one CTA per segment
+    // one CTA per segment (for a size tier: per list slot, the unused tail exits at once)
+    k_segment_sort<KIND, BLOCK, ITEMS, MODE><<<count, BLOCK, sm, st>>>(lv);
 }
 
-// big / small CTA configurations per kind
-// (overridable with -D for tuning experiments)
-#ifndef GBS_KEYS_BLOCK
-#define GBS_KEYS_BLOCK 1024
-#define GBS_KEYS_ITEMS 32
-#endif
-#ifndef GBS_WIDE_BLOCK
-#define GBS_WIDE_BLOCK 1024
-#define GBS_WIDE_ITEMS 16
-#endif
-#define GBS_BIG_KEYS GBS_KEYS_BLOCK, GBS_KEYS_ITEMS
-#define GBS_BIG_WIDE GBS_WIDE_BLOCK, GBS_WIDE_ITEMS
-#ifndef GBS_SMALL
-#define GBS_SMALL 256, 8
-#endif
 
 template <int KIND>
 static void launch_local(const LevelDev& lv, bool small, cudaStream_t st)
@@ -485,16 +510,40 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
         constexpr uint32_t TILE = tile_of_c(KIND);
         constexpr int ITEMS = KIND == KIND_KEYS ? GBS_KEYS_ITEMS : GBS_WIDE_ITEMS;
         if (GBS_SPLIT_STEP9_ON && split_step9(KIND, nd)) {
-            // buckets of at most half a tile go to a 512-thread CTA (2 per SM: one's
-            // load/store phases overlap the other's sort); larger ones to 1024 threads
-            LevelDev lo = lv, hi = lv;
-            lo.seg_max = TILE / 2;
-            hi.seg_min = TILE / 2;
-            launch_seg_t<KIND, 512, ITEMS, MODE_BUCKET>(lo, nd.B * nd.s, st);
+            // Size tiers: buckets of at most half a tile on 512-thread CTAs (2 per SM:
+            // one's load/store phases overlap the other's sort); those a little over half
+            // a tile (common: the average bucket n/s is about half the tight bound) on
+            // a 5/8-tile configuration (keys: 512 threads, still 2 CTAs per SM); the rare larger ones
+            // on the full tile.  Each tier launches over the list k_bucket_tiers builds.
+            const uint32_t count = nd.B * nd.s;
+            uint32_t* lists = reinterpret_cast<uint32_t*>(ws + nd.o_tiers);
+            uint32_t* lens = lists + 3 * (uint64_t)count;
+            const uint32_t cut1 = GBS_MID_STEP9 ? mid_cap(KIND) : TILE;
+            GBS_CUDA(cudaMemsetAsync(lens, 0, 16, st));
+            k_bucket_tiers<<<(count + 255) / 256, 256, 0, st>>>(lv, lists, lens, TILE / 2, cut1);
             GBS_LAUNCHED();
-            if constexpr (KIND == KIND_KEYS) launch_seg_t<KIND, GBS_BIG_KEYS, MODE_BUCKET>(hi, nd.B * nd.s, st);
-            else launch_seg_t<KIND, GBS_BIG_WIDE, MODE_BUCKET>(hi, nd.B * nd.s, st);
+            LevelDev t0 = lv, t1 = lv, t2 = lv;
+            t0.tier_list = lists;
+            t0.tier_len = lens;
+            t1.tier_list = lists + count;
+            t1.tier_len = lens + 1;
+            t2.tier_list = lists + 2 * (uint64_t)count;
+            t2.tier_len = lens + 2;
+            launch_seg_t<KIND, 512, ITEMS, MODE_BUCKET>(t0, count, st);
             GBS_LAUNCHED();
+            if (GBS_MID_STEP9) {
+                launch_seg_t<KIND, MID_BLOCK_OF(KIND), MID_ITEMS_OF(KIND), MODE_BUCKET>(t1, count, st);
+                GBS_LAUNCHED();
+                if (nd.hi > cut1) {
+                    if constexpr (KIND == KIND_KEYS) launch_seg_t<KIND, GBS_BIG_KEYS, MODE_BUCKET>(t2, count, st);
+                    else launch_seg_t<KIND, GBS_BIG_WIDE, MODE_BUCKET>(t2, count, st);
+                    GBS_LAUNCHED();
+                }
+            } else {
+                if constexpr (KIND == KIND_KEYS) launch_seg_t<KIND, GBS_BIG_KEYS, MODE_BUCKET>(t1, count, st);
+                else launch_seg_t<KIND, GBS_BIG_WIDE, MODE_BUCKET>(t1, count, st);
+                GBS_LAUNCHED();
+            }
         } else {
             launch_seg<KIND, MODE_BUCKET>(lv, nd.bucket_small, nd.B * nd.s, st);
         }

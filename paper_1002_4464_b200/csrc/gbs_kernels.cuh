@@ -57,6 +57,10 @@ struct LevelDev {
     uint32_t pf_stride;    // co-resident CTAs (SMs x CTAs/SM): CTA b prefetches CTA b + pf_stride
     uint32_t presorted;    // input consists of sorted runs of this length (Step 4 levels), 0 = none
     uint32_t seg_min, seg_max;   // k_segment_sort: this launch sorts segments of seg_min < v <= seg_max
+    // k_segment_sort over a size tier: the tier's bucket list (k_bucket_tiers) and its
+    // length; null = one CTA per segment of the level
+    const uint32_t* tier_list;
+    const uint32_t* tier_len;
 };
 
 // L2 prefetch of a byte range (cp.async.bulk.prefetch: a TMA bulk operation, no
@@ -838,6 +842,23 @@ __device__ __forceinline__ void segment_of(const LevelDev& lv, uint32_t idx, uin
     }
 }
 
+// Step 9 size tiers: bucket idx goes to list t (0: 0 < v <= cut0, 1: cut0 < v <= cut1,
+// 2: v > cut1); empty buckets are dropped.  The order inside a list is arbitrary (each
+// bucket is sorted on its own, so the output does not depend on it).
+__global__ void k_bucket_tiers(LevelDev lv, uint32_t* lists, uint32_t* lens, uint32_t cut0, uint32_t cut1)
+{
+    const uint32_t count = lv.B * lv.s;
+    const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= count) return;
+    uint64_t off;
+    int v;
+    segment_of<MODE_BUCKET>(lv, idx, off, v);
+    if (v <= 0) return;
+    const uint32_t t = (uint32_t)v <= cut0 ? 0u : ((uint32_t)v <= cut1 ? 1u : 2u);
+    const uint32_t pos = atomicAdd(lens + t, 1u);
+    lists[(uint64_t)t * count + pos] = idx;
+}
+
 // One CTA per segment (bucket or leaf problem), adaptive tile size.  The segment
 // pf_stride ahead (the next wave) is prefetched into L2.  (A persistent variant that
 // walked segments with a work counter and register prefetch measured ~8% slower: the
@@ -845,17 +866,37 @@ __device__ __forceinline__ void segment_of(const LevelDev& lv, uint32_t idx, uin
 template <int KIND, int BLOCK, int ITEMS, int MODE>
 __global__ void __launch_bounds__(BLOCK, (BLOCK <= 512 ? 2 : 1)) k_segment_sort(LevelDev lv)
 {
-    using A = Adapt<KIND, BLOCK, ITEMS, GBS_ADAPT_DEPTH>;
+    // the mid tier (ITEMS not a power of two) only sees sizes just above the small tier
+    using A = Adapt<KIND, BLOCK, ITEMS, ((ITEMS & (ITEMS - 1)) == 0 ? GBS_ADAPT_DEPTH : 0)>;
     using KeyT = typename A::S::KeyT;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const void* src = MODE == MODE_LEAF ? lv.in : lv.reloc;
     const uint32_t* src_v = MODE == MODE_LEAF ? lv.in_v : lv.reloc_v;
+    if (lv.tier_list) {
+        // one size tier: CTA q sorts the q-th bucket of the tier's list (k_bucket_tiers);
+        // the CTAs past the list's length exit at once -- they are the grid's tail, so
+        // the hardware block scheduler still balances the real buckets over the SMs
+        const uint32_t len = *lv.tier_len;
+        if (blockIdx.x >= len) return;
+        if (threadIdx.x == 0 && blockIdx.x + lv.pf_stride < len) {
+            uint64_t po;
+            int pv;
+            segment_of<MODE>(lv, lv.tier_list[blockIdx.x + lv.pf_stride], po, pv);
+            prefetch_l2(reinterpret_cast<const KeyT*>(src) + po, (size_t)pv * sizeof(KeyT));
+            if (KIND == KIND_PAIRS) prefetch_l2(src_v + po, (size_t)pv * 4);
+        }
+        uint64_t off;
+        int v;
+        segment_of<MODE>(lv, lv.tier_list[blockIdx.x], off, v);
+        A::run(src, src_v, off, v, lv.out, lv.out_v, smem_raw);
+        return;
+    }
     const uint32_t count = MODE == MODE_LEAF ? lv.B : lv.B * lv.s;
     if (threadIdx.x == 0 && blockIdx.x + lv.pf_stride < count) {
         uint64_t po;
         int pv;
         segment_of<MODE>(lv, blockIdx.x + lv.pf_stride, po, pv);
-        if (pv > 0) {
+        if (pv > 0 && (uint32_t)pv > lv.seg_min && (uint32_t)pv <= lv.seg_max) {   // this launch's
             prefetch_l2(reinterpret_cast<const KeyT*>(src) + po, (size_t)pv * sizeof(KeyT));
             if (KIND == KIND_PAIRS) prefetch_l2(src_v + po, (size_t)pv * 4);
         }

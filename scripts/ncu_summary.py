@@ -60,8 +60,19 @@ def main():
                             round(v, 3)) for v, h in stalls[:6]]
         d["dram_bytes_per_launch"] = d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0)
         d["duration_us"] = d.get("gpu__time_duration.sum")
+        prev = out["all"][-1]["kernel"] if out["all"] else None
         out["all"].append(d)
-        out["kernels"].setdefault(base, d)
+        first = out["kernels"].get(base)
+        if first is None:
+            out["kernels"][base] = dict(d, launches=1, parts=[name])
+        elif prev is not None and prev.split("<")[0] == name.split("<")[0] \
+                and prev.split(",")[0] == name.split(",")[0] and first["parts"][-1] == prev:
+            # a step issued as back-to-back launches of one kernel and item kind (Step 9's
+            # split by bucket size): the step's traffic and time are their sum
+            first["dram_bytes_per_launch"] += d["dram_bytes_per_launch"]
+            first["duration_us"] = (first["duration_us"] or 0) + (d["duration_us"] or 0)
+            first["launches"] += 1
+            first["parts"].append(name)
     js = json.dumps(out, indent=1)
     if len(sys.argv) > 2:
         open(sys.argv[2], "w").write(js)

@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--dist", default="uniform")
     ap.add_argument("--impl", default="gbs", choices=["gbs", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--n", type=int, default=0, help="override the workload's size (experiments; not a bench line)")
     ap.add_argument("--force-dist", action="store_true",
                     help="use the multi-GPU entry even with one rank (exercises E1-E9 on one GPU)")
     return ap.parse_args()
@@ -235,6 +236,8 @@ def main():
         dist.barrier()
 
     n, wl = WORKLOADS[args.workload]
+    if args.n:
+        n, wl = args.n, f"{args.workload} shape at n={args.n} (size override)"
     stream = torch.cuda.current_stream()
     # rank r holds global elements [r n, (r+1) n) of an N = world*n array
     if args.dist == "sorted":

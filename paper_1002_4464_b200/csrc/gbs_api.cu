@@ -82,6 +82,12 @@ constexpr uint32_t SMALL_TILE = 2048;      // small CTA configuration
 #ifndef GBS_SPLIT_STEP9
 #define GBS_SPLIT_STEP9 1
 #endif
+#ifndef GBS_FUSE_89
+#define GBS_FUSE_89 1     // fused Step 8+9 for CTA-bucket levels
+#endif
+#ifndef GBS_FUSE_MIN_D
+#define GBS_FUSE_MIN_D 32 // ... whose average run d = L/s is at least this many items
+#endif
 constexpr bool GBS_SPLIT_STEP9_ON = GBS_SPLIT_STEP9;
 constexpr uint64_t SMALL_U64_TOTAL = 1u << 18;   // u64 levels up to this many samples use 2K tiles
 constexpr uint32_t D_MIN = 8;              // single level needs d >= 8
@@ -112,6 +118,8 @@ struct Node {
     size_t o_samples = 0, o_splitters = 0, o_a = 0, o_l = 0, o_state = 0;
     size_t o_child_off = 0, o_child_len = 0, o_reloc = SIZE_MAX, o_reloc_v = SIZE_MAX;
     size_t o_tiers = 0;   // Step 9 size-tier lists (3 x B*s) + counters (4)
+    size_t o_pex = 0;     // fused Step 8+9: run starts P_i,j-1 (B*m*s)
+    bool fuse89 = false;  // Step 9 gathers straight from the sorted sublists (no Step 8 pass)
 };
 
 // big / small CTA configurations per kind
@@ -229,7 +237,7 @@ static int build_node(Plan& P, int kind, uint32_t B, uint64_t N, uint32_t pad_ba
         nd.o_reloc = P.alloc((uint64_t)B * N * key_bytes(kind));
         if (kind == KIND_PAIRS) nd.o_reloc_v = P.alloc((uint64_t)B * N * 4);
     }
-    P.launches += 4;  // local sort (+samples), sample index (+splitters), scan, relocate
+    P.launches += 3;  // local sort (+samples), sample index (+splitters), scan
     const int idx = (int)P.nodes.size();
     P.nodes.push_back(nd);
     const uint32_t child_pad = kind == KIND_U64 ? pad_base + (uint32_t)(nd.Np - N) : (uint32_t)nd.Np;
@@ -242,10 +250,23 @@ static int build_node(Plan& P, int kind, uint32_t B, uint64_t N, uint32_t pad_ba
         P.launches += step9_launches(kind, P.nodes[idx]);
         if (GBS_SPLIT_STEP9_ON && split_step9(kind, P.nodes[idx]))
             P.nodes[idx].o_tiers = P.alloc(((uint64_t)B * s * 3 + 4) * 4);
+        // fused Step 8+9 when the bucket's m run descriptors fit the staging area
+        // (a production call; stop_after_step runs keep the explicit Step 8)
+        // (keys only for now: the 16-item u64 / pair gather variants spill registers)
+        // and the runs are long enough (d = L/s items on average) for the gathered reads
+        // not to over-fetch: at d = 16 (64-byte runs) the scattered reads cost what the
+        // relocation pass costs (measured); at d >= 32 and on small inputs the fused path wins
+        if (GBS_FUSE_89 && kind == KIND_KEYS && P.nodes[idx].m <= gather_max_m(kind) &&
+            P.nodes[idx].d >= GBS_FUSE_MIN_D) {
+            P.nodes[idx].fuse89 = true;
+            P.nodes[idx].o_pex = P.alloc(ms * 4);
+        } else {
+            P.launches += 1;  // relocate
+        }
     } else {
         P.nodes[idx].o_child_off = P.alloc((uint64_t)B * s * 8);
         P.nodes[idx].o_child_len = P.alloc((uint64_t)B * s * 4);
-        P.launches += 1;
+        P.launches += 2;  // relocate + child descriptors
         const uint64_t nb = (uint64_t)B * s;
         if (nb >= (1ull << 31)) { snprintf(g_err, sizeof g_err, "too many nested problems"); return -1; }
         const int c9 = build_node(P, kind, (uint32_t)nb, nd.hi, child_pad, nullptr, false);
@@ -275,6 +296,12 @@ static gbs_status_t make_plan(size_t n, int kind, const gbs_config_t* cfg, Plan&
 static uint32_t num_sms();
 #ifndef GBS_SPLIT_STEP9
 #define GBS_SPLIT_STEP9 1
+#endif
+#ifndef GBS_FUSE_89
+#define GBS_FUSE_89 1     // fused Step 8+9 for CTA-bucket levels
+#endif
+#ifndef GBS_FUSE_MIN_D
+#define GBS_FUSE_MIN_D 32 // ... whose average run d = L/s is at least this many items
 #endif
 #ifndef GBS_IDX_TMA
 #define GBS_IDX_TMA 1
@@ -306,7 +333,10 @@ static void launch_local_t(const LevelDev& lv0, cudaStream_t st)
 template <int KIND, int BLOCK, int ITEMS, int MODE>
 static void launch_seg_t(const LevelDev& lv, unsigned count, cudaStream_t st)
 {
-    const size_t sm = Seg<KIND, BLOCK, ITEMS>::smem_bytes();
+    // the fused Step 8+9 stages its run table (m + 1 uint2) behind the tile
+    const size_t sm = MODE == MODE_GATHER
+                          ? gather_smem_offset<KIND, BLOCK, ITEMS>() + ((size_t)gather_max_m(KIND) + 1) * 8
+                          : Seg<KIND, BLOCK, ITEMS>::smem_bytes();
     static std::once_flag f;
     static int occ = 1;
     std::call_once(f, [&] {
@@ -381,6 +411,22 @@ static uint32_t num_sms()
     return (uint32_t)n;
 }
 
+// A second stream per device for work that runs beside the call's stream inside one
+// step (fork/join through events, so the call stays ordered on the caller's stream;
+// capturable into a CUDA graph).  Shared by concurrent calls: that only serialises the
+// side work, the dependencies stay per call.
+static cudaStream_t side_stream()
+{
+    static std::mutex mu;
+    static cudaStream_t ss[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(mu);
+    if (dev < 0 || dev >= 64) return nullptr;
+    if (!ss[dev] && cudaStreamCreateWithFlags(&ss[dev], cudaStreamNonBlocking) != cudaSuccess) ss[dev] = nullptr;
+    return ss[dev];
+}
+
 struct Bufs {
     void *in, *reloc, *out;
     uint32_t *in_v, *reloc_v, *out_v;
@@ -396,6 +442,75 @@ static gbs_status_t exec(const Plan& P, int ni, char* ws, const Bufs& bf, Probs 
         case KIND_PAIRS: return exec_kind<KIND_PAIRS>(P, ni, ws, bf, pr, st, stop);
         default: return exec_kind<KIND_U64>(P, ni, ws, bf, pr, st, stop);
     }
+}
+
+// Step 9 over CTA buckets: one launch, or the size tiers (MODE_BUCKET reads the
+// relocated buckets, MODE_GATHER gathers them from the sorted sublists)
+template <int KIND, int MODE>
+static gbs_status_t launch_step9(const LevelDev& lv, const Node& nd, char* ws, cudaStream_t st)
+{
+    {
+        constexpr uint32_t TILE = tile_of_c(KIND);
+        constexpr int ITEMS = KIND == KIND_KEYS ? GBS_KEYS_ITEMS : GBS_WIDE_ITEMS;
+        if (GBS_SPLIT_STEP9_ON && split_step9(KIND, nd)) {
+            // Size tiers: buckets of at most half a tile on 512-thread CTAs (2 per SM:
+            // one's load/store phases overlap the other's sort); those a little over half
+            // a tile (common: the average bucket n/s is about half the tight bound) on a
+            // 5/8-tile configuration (keys: 512 threads, still 2 CTAs per SM); the rare
+            // larger ones on the full tile.  Each tier launches over its list (built by
+            // k_bucket_tiers).
+            const uint32_t count = nd.B * nd.s;
+            uint32_t* lists = reinterpret_cast<uint32_t*>(ws + nd.o_tiers);
+            uint32_t* lens = lists + 3 * (uint64_t)count;
+            const uint32_t cut1 = GBS_MID_STEP9 ? mid_cap(KIND) : TILE;
+            GBS_CUDA(cudaMemsetAsync(lens, 0, 16, st));
+            k_bucket_tiers<<<(count + 255) / 256, 256, 0, st>>>(lv, lists, lens, TILE / 2, cut1);
+            GBS_LAUNCHED();
+            LevelDev t0 = lv, t1 = lv, t2 = lv;
+            t0.tier_list = lists;
+            t0.tier_len = lens;
+            t1.tier_list = lists + count;
+            t1.tier_len = lens + 1;
+            t2.tier_list = lists + 2 * (uint64_t)count;
+            t2.tier_len = lens + 2;
+            // The tiers run concurrently: the larger tiers (few CTAs, each a full-tile
+            // sort) on the side stream, so they are not a serial tail after tier 0.
+            cudaStream_t ss = side_stream();
+            cudaEvent_t fork = nullptr, join = nullptr;
+            if (ss) {
+                GBS_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+                GBS_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+                GBS_CUDA(cudaEventRecord(fork, st));
+                GBS_CUDA(cudaStreamWaitEvent(ss, fork, 0));
+            }
+            cudaStream_t s12 = ss ? ss : st;
+            if (GBS_MID_STEP9) {
+                if (nd.hi > cut1) {
+                    if constexpr (KIND == KIND_KEYS) launch_seg_t<KIND, GBS_BIG_KEYS, MODE>(t2, count, s12);
+                    else launch_seg_t<KIND, GBS_BIG_WIDE, MODE>(t2, count, s12);
+                    GBS_LAUNCHED();
+                }
+                launch_seg_t<KIND, MID_BLOCK_OF(KIND), MID_ITEMS_OF(KIND), MODE>(t1, count, s12);
+                GBS_LAUNCHED();
+            } else {
+                if constexpr (KIND == KIND_KEYS) launch_seg_t<KIND, GBS_BIG_KEYS, MODE>(t1, count, s12);
+                else launch_seg_t<KIND, GBS_BIG_WIDE, MODE>(t1, count, s12);
+                GBS_LAUNCHED();
+            }
+            launch_seg_t<KIND, 512, ITEMS, MODE>(t0, count, st);
+            GBS_LAUNCHED();
+            if (ss) {
+                GBS_CUDA(cudaEventRecord(join, ss));
+                GBS_CUDA(cudaStreamWaitEvent(st, join, 0));
+                cudaEventDestroy(fork);
+                cudaEventDestroy(join);
+            }
+        } else {
+            launch_seg<KIND, MODE>(lv, nd.bucket_small, nd.B * nd.s, st);
+        }
+        GBS_LAUNCHED();
+    }
+    return GBS_SUCCESS;
 }
 
 template <int KIND>
@@ -432,6 +547,19 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
     lv.a = reinterpret_cast<uint32_t*>(ws + nd.o_a);
     lv.l = reinterpret_cast<uint32_t*>(ws + nd.o_l);
     lv.state = reinterpret_cast<unsigned long long*>(ws + nd.o_state);
+    // fused Step 8+9: Step 2 must not sort in place when the output is the input (the
+    // bucket CTAs would overwrite runs other CTAs still gather), so it writes the sorted
+    // sublists to the reloc buffer, which Step 8 no longer needs
+    const bool fuse = nd.fuse89 && stop == 0;
+    lv.srt = lv.in;
+    lv.srt_v = lv.in_v;
+    if (fuse) {
+        lv.pex = reinterpret_cast<uint32_t*>(ws + nd.o_pex);
+        if (lv.in == lv.out) {
+            lv.srt = lv.reloc;
+            lv.srt_v = lv.reloc_v;
+        }
+    }
     ProfMarks pm;
     if (g_prof && ni == 0 && stop == 0) {
         std::array<cudaEvent_t, 8> evs;
@@ -499,55 +627,22 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
     if (stop == 7) return GBS_SUCCESS;
     pm.mark();
 
-    // Step 8: relocation in -> reloc
-    launch_relocate<KIND>(lv, st);
-    GBS_LAUNCHED();
+    // Step 8: relocation in -> reloc (fused into Step 9 on the production path)
+    if (!fuse) {
+        launch_relocate<KIND>(lv, st);
+        GBS_LAUNCHED();
+    }
     if (stop == 8) return GBS_SUCCESS;
     pm.mark();
 
     // Step 9: bucket sort reloc -> out (one CTA per bucket) or a nested level
     if (nd.step9 < 0) {
-        constexpr uint32_t TILE = tile_of_c(KIND);
-        constexpr int ITEMS = KIND == KIND_KEYS ? GBS_KEYS_ITEMS : GBS_WIDE_ITEMS;
-        if (GBS_SPLIT_STEP9_ON && split_step9(KIND, nd)) {
-            // Size tiers: buckets of at most half a tile on 512-thread CTAs (2 per SM:
-            // one's load/store phases overlap the other's sort); those a little over half
-            // a tile (common: the average bucket n/s is about half the tight bound) on
-            // a 5/8-tile configuration (keys: 512 threads, still 2 CTAs per SM); the rare larger ones
-            // on the full tile.  Each tier launches over the list k_bucket_tiers builds.
-            const uint32_t count = nd.B * nd.s;
-            uint32_t* lists = reinterpret_cast<uint32_t*>(ws + nd.o_tiers);
-            uint32_t* lens = lists + 3 * (uint64_t)count;
-            const uint32_t cut1 = GBS_MID_STEP9 ? mid_cap(KIND) : TILE;
-            GBS_CUDA(cudaMemsetAsync(lens, 0, 16, st));
-            k_bucket_tiers<<<(count + 255) / 256, 256, 0, st>>>(lv, lists, lens, TILE / 2, cut1);
-            GBS_LAUNCHED();
-            LevelDev t0 = lv, t1 = lv, t2 = lv;
-            t0.tier_list = lists;
-            t0.tier_len = lens;
-            t1.tier_list = lists + count;
-            t1.tier_len = lens + 1;
-            t2.tier_list = lists + 2 * (uint64_t)count;
-            t2.tier_len = lens + 2;
-            launch_seg_t<KIND, 512, ITEMS, MODE_BUCKET>(t0, count, st);
-            GBS_LAUNCHED();
-            if (GBS_MID_STEP9) {
-                launch_seg_t<KIND, MID_BLOCK_OF(KIND), MID_ITEMS_OF(KIND), MODE_BUCKET>(t1, count, st);
-                GBS_LAUNCHED();
-                if (nd.hi > cut1) {
-                    if constexpr (KIND == KIND_KEYS) launch_seg_t<KIND, GBS_BIG_KEYS, MODE_BUCKET>(t2, count, st);
-                    else launch_seg_t<KIND, GBS_BIG_WIDE, MODE_BUCKET>(t2, count, st);
-                    GBS_LAUNCHED();
-                }
-            } else {
-                if constexpr (KIND == KIND_KEYS) launch_seg_t<KIND, GBS_BIG_KEYS, MODE_BUCKET>(t1, count, st);
-                else launch_seg_t<KIND, GBS_BIG_WIDE, MODE_BUCKET>(t1, count, st);
-                GBS_LAUNCHED();
-            }
-        } else {
-            launch_seg<KIND, MODE_BUCKET>(lv, nd.bucket_small, nd.B * nd.s, st);
-        }
-        GBS_LAUNCHED();
+        gbs_status_t r9;
+        if constexpr (KIND == KIND_KEYS)
+            r9 = fuse ? launch_step9<KIND, MODE_GATHER>(lv, nd, ws, st) : launch_step9<KIND, MODE_BUCKET>(lv, nd, ws, st);
+        else
+            r9 = launch_step9<KIND, MODE_BUCKET>(lv, nd, ws, st);
+        if (r9) return r9;
     } else {
         lv.child_off = reinterpret_cast<u64*>(ws + nd.o_child_off);
         lv.child_len = reinterpret_cast<uint32_t*>(ws + nd.o_child_len);

@@ -61,6 +61,11 @@ struct LevelDev {
     // length; null = one CTA per segment of the level
     const uint32_t* tier_list;
     const uint32_t* tier_len;
+    // where Step 2 writes the sorted sublists (Steps 3, 6, 8 and the fused Step 8+9 read
+    // them): `in` itself, or -- for the fused path when in == out -- the reloc buffer
+    void* srt;
+    uint32_t* srt_v;
+    uint32_t* pex;        // fused Step 8+9: P_i,j-1 (run start in sublist i), row-major like a
 };
 
 // L2 prefetch of a byte range (cp.async.bulk.prefetch: a TMA bulk operation, no
@@ -154,7 +159,7 @@ struct Seg {
     using CS = CtaSort<T, BLOCK, ITEMS, (KIND == KIND_KEYS ? GBS_KEYS_CHAINS : GBS_WIDE_CHAINS)>;
     using KeyT = typename std::conditional<KIND == KIND_U64, unsigned long long, uint32_t>::type;  // in HBM
     static constexpr int TILE = CS::TILE;
-    static constexpr size_t smem_bytes()
+    __host__ __device__ static constexpr size_t smem_bytes()
     {
         return sizeof(T) * CS::SMEM_ELEMS + (KIND == KIND_PAIRS ? sizeof(uint32_t) * TILE : 0);
     }
@@ -183,6 +188,53 @@ struct Seg {
         }
     }
 
+    // Fused Step 8+9: register slot k holds bucket position load_pos(k) (32 consecutive
+    // positions per warp instruction, as for a relocated bucket, so the reads stay
+    // coalesced inside each run).  Each lane finds the run of its first position by
+    // binary search over the run table, then walks forward (positions only grow).
+    // Pairs carry the position p as the tie-break and park the value in vsm[p], exactly
+    // as load_regs does for a relocated bucket.
+    template <int M, typename G>
+    static __device__ __forceinline__ void load_gather(T (&x)[M], const G& g, int v, unsigned char* smem)
+    {
+        const int pbase = CS::load_pos(0);            // + 32 k
+        int i = 0;
+        if (pbase < v) {
+            int lo = 0, hi = g.m - 1;                 // last run i with start_i <= pbase
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if ((int)g.run[mid].x <= pbase) lo = mid;
+                else hi = mid - 1;
+            }
+            i = lo;
+        }
+        uint32_t base = g.run[i].y;
+        uint2 nx = g.run[i + 1];
+        uint32_t* vsm = KIND == KIND_PAIRS ? vsm_of(smem) : nullptr;
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k) {
+            const int p = pbase + 32 * k;
+            if (p < v) {
+                while (p >= (int)nx.x) {              // next non-empty run
+                    base = nx.y;
+                    ++i;
+                    nx = g.run[i + 1];
+                }
+                const uint32_t q = base + (uint32_t)p;
+                if constexpr (KIND == KIND_PAIRS) {
+                    const uint32_t key = __ldg(reinterpret_cast<const uint32_t*>(g.src) + q);
+                    x[k] = ((T)key << 32) | (T)(uint32_t)p;
+                    vsm[p] = __ldg(g.src_v + q);
+                } else {
+                    x[k] = (T)__ldg(reinterpret_cast<const KeyT*>(g.src) + q);
+                }
+            } else {
+                if constexpr (KIND == KIND_PAIRS) x[k] = ((T)0xFFFFFFFFu << 32) | (T)(uint32_t)p;
+                else x[k] = CS::TMAX;
+            }
+        }
+    }
+
     static __device__ __forceinline__ void store(void* dst, uint32_t* dst_v, uint64_t dst_off, int v,
                                                  unsigned char* smem)
     {
@@ -204,6 +256,22 @@ struct Seg {
             for (int p = threadIdx.x; p < v; p += BLOCK) d[p] = sm[CS::phys(p)];
         }
     }
+};
+
+// Fused Step 8+9: where bucket j's items come from.  Relocation (Step 8,
+// P:235-239) would copy run (i, j) -- the a_ij items of sorted sublist i starting at
+// P_i,j-1 -- to R[l_ij + q]; the bucket's CTA instead reads position p of B_j (in R's
+// order) straight from the sorted sublists: run i covers positions [lrel_i, lrel_i+1)
+// with lrel_i = l_ij - l_0j, and position p is sorted-sublist item i*L + P_i,j-1 +
+// (p - lrel_i).  The run table is staged in shared memory behind the tile.
+struct GatherSrc {
+    const void* src;          // sorted sublists of the bucket's problem (item 0 of sublist 0)
+    const uint32_t* src_v;
+    // run table in shared memory, m + 1 entries: x = lrel_i (run i's first bucket
+    // position; x of entry m = |B_j|), y = i*L + P_i,j-1 - lrel_i, so that bucket position
+    // p of run i is item y + p of the problem (32-bit modular: a problem has < 2^32 items)
+    const uint2* run;
+    int m;
 };
 
 // The same CTA sorts a tile of v items with ITEMS, ITEMS/2 or ITEMS/4 items per thread
@@ -239,6 +307,19 @@ struct Adapt {
         if constexpr (HALF) {
             if (v <= S::TILE / 2) { Sub::store(dst, dst_v, off, v, smem); return; }
         }
+        S::store(dst, dst_v, off, v, smem);
+    }
+    // fused Step 8+9: gather + sort + store, register array sized for the chosen tile
+    template <typename G>
+    static __device__ __forceinline__ void run_gather(const G& g, int v, void* dst, uint32_t* dst_v, uint64_t off,
+                                                      unsigned char* smem)
+    {
+        if constexpr (HALF) {
+            if (v <= S::TILE / 2) { Sub::run_gather(g, v, dst, dst_v, off, smem); return; }
+        }
+        T x[ITEMS];
+        S::load_gather(x, g, v, smem);
+        S::CS::sort(x, reinterpret_cast<T*>(smem), v);
         S::store(dst, dst_v, off, v, smem);
     }
     // load + sort + store with a register array sized for the chosen tile
@@ -308,7 +389,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_local_sort(LevelDev lv)
             }
         }
         if (pipe && nv > 0) S::load_regs(x, lv.in, lv.in_v, nstart, nv, smem_raw);   // in flight during the store
-        if (v > 0) S::store(lv.in, lv.in_v, start, v, smem_raw);
+        if (v > 0) S::store(lv.srt, lv.srt_v, start, v, smem_raw);
         u64* smp = lv.samples + ((uint64_t)b * lv.m + i) * lv.s;
         for (uint32_t k = threadIdx.x; k < lv.s; k += BLOCK) {
             const uint32_t r = (k + 1) * lv.d - 1;
@@ -399,7 +480,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_sample_index_tma(LevelDev lv)
         const int v = tile_v(t);
         const int cl = min(CH, v - c * CH);
         const unsigned bytes = (unsigned)((size_t)cl * sizeof(KT)) & ~15u;
-        const KT* src = reinterpret_cast<const KT*>(lv.in) + lv.pr.offset(t / lv.m) + (uint64_t)(t % lv.m) * lv.L +
+        const KT* src = reinterpret_cast<const KT*>(lv.srt) + lv.pr.offset(t / lv.m) + (uint64_t)(t % lv.m) * lv.L +
                         (uint64_t)c * CH;
         unsigned long long* bar = &bars[slot];
         mbar_expect_tx(bar, bytes);
@@ -459,7 +540,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_sample_index_tma(LevelDev lv)
         const int cl = min(CH, v - c0);
         {   // keys past the last 16-byte boundary of the chunk (tail of the sublist)
             const int full = (int)(((unsigned)((size_t)cl * sizeof(KT)) & ~15u) / sizeof(KT));
-            const KT* src = reinterpret_cast<const KT*>(lv.in) + lv.pr.offset(b) + i0 + c0;
+            const KT* src = reinterpret_cast<const KT*>(lv.srt) + lv.pr.offset(b) + i0 + c0;
             for (int p = full + threadIdx.x; p < cl; p += BLOCK) ks[p] = src[p];
         }
         __syncthreads();
@@ -493,6 +574,10 @@ __global__ void __launch_bounds__(BLOCK, 1) k_sample_index_tma(LevelDev lv)
             __syncthreads();
             uint32_t* arow = lv.a + ((uint64_t)b * lv.m + i) * lv.s;
             for (uint32_t j = threadIdx.x; j < lv.s; j += BLOCK) arow[j] = Q[j] - (j ? Q[j - 1] : 0u);
+            if (lv.pex) {             // fused Step 8+9: run (i, j) starts at P_i,j-1
+                uint32_t* prow = lv.pex + ((uint64_t)b * lv.m + i) * lv.s;
+                for (uint32_t j = threadIdx.x; j < lv.s; j += BLOCK) prow[j] = j ? Q[j - 1] : 0u;
+            }
             // empty sublists skipped on the way to the next tile get rows of zeros
             for (uint32_t t2 = tile + gridDim.x; t2 < ntile && t2 < ntiles; t2 += gridDim.x) {
                 uint32_t* zrow = lv.a + (uint64_t)t2 * lv.s;
@@ -523,12 +608,12 @@ __global__ void __launch_bounds__(BLOCK, 2) k_sample_index(LevelDev lv)
     const uint64_t i0 = (uint64_t)i * lv.L;
     const int v = len > i0 ? (int)umin64(len - i0, lv.L) : 0;
 
-    const KT* src = reinterpret_cast<const KT*>(lv.in) + off + i0;
+    const KT* src = reinterpret_cast<const KT*>(lv.srt) + off + i0;
     if (threadIdx.x == 0 && blockIdx.x + lv.pf_stride < lv.B * lv.m) {
         uint64_t ps;
         int pv;
         sublist_of(lv, blockIdx.x + lv.pf_stride, ps, pv);
-        prefetch_l2(reinterpret_cast<const KT*>(lv.in) + ps, (size_t)pv * sizeof(KT));
+        prefetch_l2(reinterpret_cast<const KT*>(lv.srt) + ps, (size_t)pv * sizeof(KT));
     }
     // Step 5 fused into the prologue (the paper loads the s global samples into shared
     // memory here): g_j = sorted_samples[(j+1)m - 1]; sublist 0 of each
@@ -572,6 +657,10 @@ __global__ void __launch_bounds__(BLOCK, 2) k_sample_index(LevelDev lv)
     __syncthreads();   // Q complete (also when v == 0 and the chunk loop never ran)
     uint32_t* arow = lv.a + ((uint64_t)b * lv.m + i) * lv.s;
     for (uint32_t j = threadIdx.x; j < lv.s; j += BLOCK) arow[j] = Q[j] - (j ? Q[j - 1] : 0u);
+    if (lv.pex) {                     // fused Step 8+9: run (i, j) starts at P_i,j-1
+        uint32_t* prow = lv.pex + ((uint64_t)b * lv.m + i) * lv.s;
+        for (uint32_t j = threadIdx.x; j < lv.s; j += BLOCK) prow[j] = j ? Q[j - 1] : 0u;
+    }
 }
 
 // ------------------------------------------------------------ Step 7
@@ -731,13 +820,13 @@ __global__ void __launch_bounds__(BLOCK, 2) k_relocate(LevelDev lv)
     if (v == 0) return;
 
     // prefetch the sublist (striped: r = t + k*BLOCK) -- latency overlaps the map build
-    const KT* src = reinterpret_cast<const KT*>(lv.in) + off + i0;
+    const KT* src = reinterpret_cast<const KT*>(lv.srt) + off + i0;
     if (threadIdx.x == 0 && blockIdx.x + lv.pf_stride < lv.B * lv.m) {
         uint64_t ps;
         int pv;
         sublist_of(lv, blockIdx.x + lv.pf_stride, ps, pv);
-        prefetch_l2(reinterpret_cast<const KT*>(lv.in) + ps, (size_t)pv * sizeof(KT));
-        if (KIND == KIND_PAIRS) prefetch_l2(lv.in_v + ps, (size_t)pv * 4);
+        prefetch_l2(reinterpret_cast<const KT*>(lv.srt) + ps, (size_t)pv * sizeof(KT));
+        if (KIND == KIND_PAIRS) prefetch_l2(lv.srt_v + ps, (size_t)pv * 4);
     }
 
     // the first batch of keys is loaded now; its latency overlaps the map build
@@ -794,7 +883,7 @@ __global__ void __launch_bounds__(BLOCK, 2) k_relocate(LevelDev lv)
         }
     }
     if (KIND == KIND_PAIRS) {
-        const uint32_t* sv = lv.in_v + off + i0;
+        const uint32_t* sv = lv.srt_v + off + i0;
         uint32_t* dv = lv.reloc_v + off;
         uint32_t w[U];
 #pragma unroll
@@ -823,7 +912,7 @@ __global__ void __launch_bounds__(BLOCK, 2) k_relocate(LevelDev lv)
 // Sublist sort: one CTA per bucket B_j = R[l_0j, l_0j+|B_j|),
 // |B_j| <= the tight bound <= tile capacity (checked by the planner).  MODE_LEAF:
 // one CTA per whole problem (len_b <= tile).
-enum SegMode { MODE_BUCKET = 0, MODE_LEAF = 1 };
+enum SegMode { MODE_BUCKET = 0, MODE_LEAF = 1, MODE_GATHER = 2 };   // GATHER: fused Step 8+9
 
 // Segment idx of a Step-9 / leaf launch: element offset and length.
 template <int MODE>
@@ -843,21 +932,54 @@ __device__ __forceinline__ void segment_of(const LevelDev& lv, uint32_t idx, uin
 }
 
 // Step 9 size tiers: bucket idx goes to list t (0: 0 < v <= cut0, 1: cut0 < v <= cut1,
-// 2: v > cut1); empty buckets are dropped.  The order inside a list is arbitrary (each
-// bucket is sorted on its own, so the output does not depend on it).
-__global__ void k_bucket_tiers(LevelDev lv, uint32_t* lists, uint32_t* lens, uint32_t cut0, uint32_t cut1)
+// 2: v > cut1); empty buckets are dropped.  Each 256-bucket block appends its buckets in
+// index order (ballot compaction; one atomic per tier and block), so neighbouring CTAs
+// of a tier read neighbouring runs.  The output never depends on the list order: each
+// bucket is sorted on its own.
+__global__ void __launch_bounds__(256) k_bucket_tiers(LevelDev lv, uint32_t* lists, uint32_t* lens, uint32_t cut0,
+                                                      uint32_t cut1)
 {
+    __shared__ uint32_t wcnt[3][8], wbase[3][8];
     const uint32_t count = lv.B * lv.s;
-    const uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x;
-    if (idx >= count) return;
-    uint64_t off;
-    int v;
-    segment_of<MODE_BUCKET>(lv, idx, off, v);
-    if (v <= 0) return;
-    const uint32_t t = (uint32_t)v <= cut0 ? 0u : ((uint32_t)v <= cut1 ? 1u : 2u);
-    const uint32_t pos = atomicAdd(lens + t, 1u);
-    lists[(uint64_t)t * count + pos] = idx;
+    const uint32_t idx = blockIdx.x * 256 + threadIdx.x;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int t = -1;
+    if (idx < count) {
+        uint64_t off;
+        int v;
+        segment_of<MODE_BUCKET>(lv, idx, off, v);
+        if (v > 0) t = (uint32_t)v <= cut0 ? 0 : ((uint32_t)v <= cut1 ? 1 : 2);
+    }
+    uint32_t mine = 0;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        const uint32_t mask = __ballot_sync(0xffffffffu, t == q);
+        if (lane == 0) wcnt[q][w] = __popc(mask);
+        if (t == q) mine = __popc(mask & ((1u << lane) - 1u));
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        const int q = threadIdx.x;
+        uint32_t tot = 0;
+        for (int k = 0; k < 8; ++k) { wbase[q][k] = tot; tot += wcnt[q][k]; }
+        const uint32_t base = tot ? atomicAdd(lens + q, tot) : 0u;
+        for (int k = 0; k < 8; ++k) wbase[q][k] += base;
+    }
+    __syncthreads();
+    if (t >= 0) lists[(uint64_t)t * count + wbase[t][w] + mine] = idx;
 }
+
+#ifndef GBS_GATHER_PF
+#define GBS_GATHER_PF 0   // fused Step 8+9: L2 prefetch of the next wave's runs (measured: no gain)
+#endif
+// Fused Step 8+9: lrel / pex staging area behind the CTA's largest tile
+template <int KIND, int BLOCK, int ITEMS>
+__host__ __device__ constexpr size_t gather_smem_offset()
+{
+    return (Seg<KIND, BLOCK, ITEMS>::smem_bytes() + 15) / 16 * 16;
+}
+// most sublists per problem the fused path stages (the plan falls back to Step 8 above)
+__host__ __device__ constexpr uint32_t gather_max_m(int kind) { return kind == KIND_KEYS ? 2048u : 1024u; }
 
 // One CTA per segment (bucket or leaf problem), adaptive tile size.  The segment
 // pf_stride ahead (the next wave) is prefetched into L2.  (A persistent variant that
@@ -870,6 +992,48 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK <= 512 ? 2 : 1)) k_segment_sort(
     using A = Adapt<KIND, BLOCK, ITEMS, ((ITEMS & (ITEMS - 1)) == 0 ? GBS_ADAPT_DEPTH : 0)>;
     using KeyT = typename A::S::KeyT;
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    if constexpr (MODE == MODE_GATHER) {
+        uint32_t idx = blockIdx.x;
+        if (lv.tier_list) {
+            if (blockIdx.x >= *lv.tier_len) return;
+            idx = lv.tier_list[blockIdx.x];
+        }
+        uint64_t off;
+        int v;
+        segment_of<MODE_BUCKET>(lv, idx, off, v);
+        if (v <= 0 || (!lv.tier_list && ((uint32_t)v <= lv.seg_min || (uint32_t)v > lv.seg_max))) return;
+        {
+            // L2 prefetch of the runs of the bucket pf_stride CTAs ahead (the next wave):
+            // one bulk prefetch per run, from that bucket's a and P_i,j-1 columns
+            const uint32_t q2 = blockIdx.x + lv.pf_stride;
+            const uint32_t len = lv.tier_list ? *lv.tier_len : lv.B * lv.s;
+            if (GBS_GATHER_PF && q2 < len) {
+                const uint32_t idx2 = lv.tier_list ? lv.tier_list[q2] : q2;
+                const uint32_t b2 = idx2 / lv.s, j2 = idx2 % lv.s;
+                const uint64_t c2 = (uint64_t)b2 * lv.m * lv.s + j2;
+                const KeyT* s2 = reinterpret_cast<const KeyT*>(lv.srt) + lv.pr.offset(b2);
+                for (uint32_t i = threadIdx.x; i < lv.m; i += BLOCK) {
+                    const uint32_t n2 = lv.a[c2 + (uint64_t)i * lv.s];
+                    if (n2) prefetch_l2(s2 + (uint64_t)i * lv.L + lv.pex[c2 + (uint64_t)i * lv.s], (size_t)n2 * sizeof(KeyT));
+                }
+            }
+        }
+        const uint32_t b = idx / lv.s, j = idx % lv.s;
+        uint2* run = reinterpret_cast<uint2*>(smem_raw + gather_smem_offset<KIND, BLOCK, ITEMS>());
+        const uint64_t col0 = (uint64_t)b * lv.m * lv.s + j;          // (row 0, column j) of problem b
+        const uint32_t l0 = lv.l[col0];
+        for (uint32_t i = threadIdx.x; i < lv.m; i += BLOCK) {
+            const uint32_t lr = lv.l[col0 + (uint64_t)i * lv.s] - l0;
+            run[i] = make_uint2(lr, i * lv.L + lv.pex[col0 + (uint64_t)i * lv.s] - lr);
+        }
+        if (threadIdx.x == 0) run[lv.m] = make_uint2((uint32_t)v, 0u);
+        __syncthreads();
+        const uint64_t pb = lv.pr.offset(b);
+        GatherSrc g{reinterpret_cast<const KeyT*>(lv.srt) + pb, KIND == KIND_PAIRS ? lv.srt_v + pb : nullptr, run,
+                    (int)lv.m};
+        A::run_gather(g, v, lv.out, lv.out_v, off, smem_raw);
+        return;
+    }
     const void* src = MODE == MODE_LEAF ? lv.in : lv.reloc;
     const uint32_t* src_v = MODE == MODE_LEAF ? lv.in_v : lv.reloc_v;
     if (lv.tier_list) {

@@ -415,17 +415,31 @@ static uint32_t num_sms()
 // step (fork/join through events, so the call stays ordered on the caller's stream;
 // capturable into a CUDA graph).  Shared by concurrent calls: that only serialises the
 // side work, the dependencies stay per call.
-static cudaStream_t side_stream()
+static cudaStream_t side_stream(int k = 0)   // k: 0 = Step 9 tiers, 1 = H2D, 2 = D2H
 {
     static std::mutex mu;
-    static cudaStream_t ss[64] = {};
+    static cudaStream_t ss[64][3] = {};
     int dev = 0;
     cudaGetDevice(&dev);
     std::lock_guard<std::mutex> g(mu);
-    if (dev < 0 || dev >= 64) return nullptr;
-    if (!ss[dev] && cudaStreamCreateWithFlags(&ss[dev], cudaStreamNonBlocking) != cudaSuccess) ss[dev] = nullptr;
-    return ss[dev];
+    if (dev < 0 || dev >= 64 || k < 0 || k > 2) return nullptr;
+    if (!ss[dev][k] && cudaStreamCreateWithFlags(&ss[dev][k], cudaStreamNonBlocking) != cudaSuccess) ss[dev][k] = nullptr;
+    return ss[dev][k];
 }
+
+// Host-buffer calls (gbs_sort_keys_host): the H2D copy is split into chunks of sublists
+// and Step 2 sorts each chunk as it lands; Step 9 runs in groups of buckets and each
+// group's final output range is copied back while the next groups sort.
+struct HostPipe {
+    uint32_t* h;              // pinned host keys (in and out)
+    size_t n;
+    cudaStream_t cin, cout;   // copy streams
+};
+#ifndef GBS_HOST_PIPE
+#define GBS_HOST_PIPE 1
+#endif
+constexpr uint32_t HP_CHUNK_TILES = 64;   // sublists per H2D chunk (8 MB of keys)
+constexpr uint32_t HP_GROUPS = 16;        // Step 9 bucket groups (D2H chunks)
 
 struct Bufs {
     void *in, *reloc, *out;
@@ -433,14 +447,16 @@ struct Bufs {
 };
 
 template <int KIND>
-static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, Probs pr, cudaStream_t st, int stop);
+static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, Probs pr, cudaStream_t st, int stop,
+                              const HostPipe* hp);
 
-static gbs_status_t exec(const Plan& P, int ni, char* ws, const Bufs& bf, Probs pr, cudaStream_t st, int stop)
+static gbs_status_t exec(const Plan& P, int ni, char* ws, const Bufs& bf, Probs pr, cudaStream_t st, int stop,
+                         const HostPipe* hp = nullptr)
 {
     switch (P.nodes[ni].kind) {
-        case KIND_KEYS: return exec_kind<KIND_KEYS>(P, ni, ws, bf, pr, st, stop);
-        case KIND_PAIRS: return exec_kind<KIND_PAIRS>(P, ni, ws, bf, pr, st, stop);
-        default: return exec_kind<KIND_U64>(P, ni, ws, bf, pr, st, stop);
+        case KIND_KEYS: return exec_kind<KIND_KEYS>(P, ni, ws, bf, pr, st, stop, hp);
+        case KIND_PAIRS: return exec_kind<KIND_PAIRS>(P, ni, ws, bf, pr, st, stop, hp);
+        default: return exec_kind<KIND_U64>(P, ni, ws, bf, pr, st, stop, hp);
     }
 }
 
@@ -514,7 +530,8 @@ static gbs_status_t launch_step9(const LevelDev& lv, const Node& nd, char* ws, c
 }
 
 template <int KIND>
-static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, Probs pr, cudaStream_t st, int stop)
+static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, Probs pr, cudaStream_t st, int stop,
+                              const HostPipe* hp)
 {
     const Node& nd = P.nodes[ni];
     LevelDev lv;
@@ -550,7 +567,7 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
     // fused Step 8+9: Step 2 must not sort in place when the output is the input (the
     // bucket CTAs would overwrite runs other CTAs still gather), so it writes the sorted
     // sublists to the reloc buffer, which Step 8 no longer needs
-    const bool fuse = nd.fuse89 && stop == 0;
+    const bool fuse = nd.fuse89 && stop == 0 && !hp;
     lv.srt = lv.in;
     lv.srt_v = lv.in_v;
     if (fuse) {
@@ -571,8 +588,32 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
     pm.mark();
 
     // Steps 2-3: local sort + local samples (one CTA per sublist)
-    launch_local<KIND>(lv, nd.local_small, st);
-    GBS_LAUNCHED();
+    if (hp) {
+        // chunk c of sublists is copied in on hp->cin, then sorted on st
+        cudaEvent_t ev;
+        GBS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        GBS_CUDA(cudaEventRecord(ev, st));                  // d_keys free (earlier work on st)
+        GBS_CUDA(cudaStreamWaitEvent(hp->cin, ev, 0));
+        cudaEventDestroy(ev);
+        uint32_t* dk = reinterpret_cast<uint32_t*>(lv.in);
+        for (uint32_t t0 = 0; t0 < nd.m; t0 += HP_CHUNK_TILES) {
+            const uint32_t t1 = std::min(nd.m, t0 + HP_CHUNK_TILES);
+            const size_t e0 = (size_t)t0 * nd.L, e1 = std::min(hp->n, (size_t)t1 * nd.L);
+            GBS_CUDA(cudaMemcpyAsync(dk + e0, hp->h + e0, (e1 - e0) * 4, cudaMemcpyHostToDevice, hp->cin));
+            GBS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            GBS_CUDA(cudaEventRecord(ev, hp->cin));
+            GBS_CUDA(cudaStreamWaitEvent(st, ev, 0));
+            cudaEventDestroy(ev);
+            LevelDev lc = lv;
+            lc.tile_lo = t0;
+            lc.tile_hi = t1;
+            launch_local<KIND>(lc, nd.local_small, st);
+            GBS_LAUNCHED();
+        }
+    } else {
+        launch_local<KIND>(lv, nd.local_small, st);
+        GBS_LAUNCHED();
+    }
     if (stop == 2 || stop == 3) return GBS_SUCCESS;
     pm.mark();
 
@@ -636,7 +677,39 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
     pm.mark();
 
     // Step 9: bucket sort reloc -> out (one CTA per bucket) or a nested level
-    if (nd.step9 < 0) {
+    if (hp) {
+        // groups of buckets; after buckets [0, j1) are sorted, the output prefix
+        // [0, j1 m d - V) is final: exactly j1 m samples are <= g_{j1-1}, and a sublist
+        // with c samples <= g has >= c d items <= g, so >= j1 m d items (V of them
+        // possibly virtual, V = m L - n) fall in buckets < j1 (Alg. 1 Steps 3-5)
+        const uint64_t V = (uint64_t)nd.m * nd.L - hp->n;
+        const uint32_t G = std::max(1u, nd.s / HP_GROUPS);
+        uint64_t done = 0;
+        cudaEvent_t ev;
+        for (uint32_t j0 = 0; j0 < nd.s; j0 += G) {
+            const uint32_t j1 = std::min(nd.s, j0 + G);
+            LevelDev lg = lv;
+            lg.seg_lo = j0;
+            lg.seg_hi = j1;
+            launch_seg<KIND, MODE_BUCKET>(lg, nd.bucket_small, j1 - j0, st);
+            GBS_LAUNCHED();
+            const uint64_t lo_cnt = (uint64_t)j1 * nd.m * nd.d;
+            const uint64_t upto = j1 == nd.s ? hp->n : std::min<uint64_t>(hp->n, lo_cnt > V ? lo_cnt - V : 0);
+            if (upto > done) {
+                GBS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+                GBS_CUDA(cudaEventRecord(ev, st));
+                GBS_CUDA(cudaStreamWaitEvent(hp->cout, ev, 0));
+                cudaEventDestroy(ev);
+                GBS_CUDA(cudaMemcpyAsync(hp->h + done, reinterpret_cast<uint32_t*>(lv.out) + done, (upto - done) * 4,
+                                         cudaMemcpyDeviceToHost, hp->cout));
+                done = upto;
+            }
+        }
+        GBS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        GBS_CUDA(cudaEventRecord(ev, hp->cout));
+        GBS_CUDA(cudaStreamWaitEvent(st, ev, 0));          // the call completes on st
+        cudaEventDestroy(ev);
+    } else if (nd.step9 < 0) {
         gbs_status_t r9;
         if constexpr (KIND == KIND_KEYS)
             r9 = fuse ? launch_step9<KIND, MODE_GATHER>(lv, nd, ws, st) : launch_step9<KIND, MODE_BUCKET>(lv, nd, ws, st);
@@ -856,6 +929,25 @@ gbs_status_t gbs_sort_keys_host(uint32_t* h_keys, size_t n, uint32_t* d_keys, vo
     if (r) return r;
     if (ws_bytes < need) return fail(GBS_ERROR_WORKSPACE_TOO_SMALL, "workspace %zu < %zu bytes", ws_bytes, need);
     cudaStream_t st = (cudaStream_t)stream;
+    if (GBS_HOST_PIPE && n >= ((size_t)HP_CHUNK_TILES << 15)) {
+        // pipelined: copies overlap Step 2 (chunks of sublists) and Step 9 (bucket groups)
+        Plan P;
+        r = make_plan(n, KIND_KEYS, nullptr, P);
+        if (r) return r;
+        const Node& top = P.nodes[0];
+        cudaStream_t cin = side_stream(1), cout = side_stream(2);
+        if (!top.leaf && top.step9 < 0 && top.B == 1 && cin && cout) {
+            r = check_device();
+            if (r) return r;
+            if (!d_ws || ((uintptr_t)d_ws & 255)) return fail(GBS_ERROR_INVALID_VALUE, "workspace NULL or not 256-byte aligned");
+            if (((uintptr_t)d_keys & 3)) return fail(GBS_ERROR_INVALID_VALUE, "keys must be 4-byte aligned");
+            char* w = reinterpret_cast<char*>(d_ws);
+            Bufs bf{d_keys, (void*)(w + top.o_reloc), d_keys, nullptr, nullptr, nullptr};
+            Probs pr{nullptr, nullptr, 0, (uint32_t)n};
+            HostPipe hp{h_keys, n, cin, cout};
+            return exec(P, 0, w, bf, pr, st, 0, &hp);
+        }
+    }
     GBS_CUDA(cudaMemcpyAsync(d_keys, h_keys, n * 4, cudaMemcpyHostToDevice, st));
     r = run_sort(d_keys, nullptr, n, nullptr, 0, d_ws, ws_bytes, st);
     if (r) return r;

@@ -66,6 +66,9 @@ struct LevelDev {
     void* srt;
     uint32_t* srt_v;
     uint32_t* pex;        // fused Step 8+9: P_i,j-1 (run start in sublist i), row-major like a
+    // host-pipelined calls (gbs_sort_keys_host): k_local_sort sorts tiles [tile_lo,
+    // tile_hi) and k_segment_sort the segments [seg_lo, seg_hi) of the level (0, 0 = all)
+    uint32_t tile_lo, tile_hi, seg_lo, seg_hi;
 };
 
 // L2 prefetch of a byte range (cp.async.bulk.prefetch: a TMA bulk operation, no
@@ -353,11 +356,11 @@ __global__ void __launch_bounds__(BLOCK, 1) k_local_sort(LevelDev lv)
     extern __shared__ __align__(16) unsigned char smem_raw[];
     T* sm = reinterpret_cast<T*>(smem_raw);
 
-    const uint32_t ntiles = lv.B * lv.m;
+    const uint32_t ntiles = lv.tile_hi ? lv.tile_hi : lv.B * lv.m;
     const bool presorted = KIND == KIND_U64 && GBS_PRESORTED && lv.presorted >= (uint32_t)ITEMS;
     const bool pipe = KIND != KIND_PAIRS && !presorted;
     T x[ITEMS];
-    uint32_t tile = blockIdx.x;
+    uint32_t tile = lv.tile_lo + blockIdx.x;
     uint64_t start = 0;
     int v = 0;
     if (tile < ntiles) {
@@ -1056,10 +1059,11 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK <= 512 ? 2 : 1)) k_segment_sort(
         return;
     }
     const uint32_t count = MODE == MODE_LEAF ? lv.B : lv.B * lv.s;
-    if (threadIdx.x == 0 && blockIdx.x + lv.pf_stride < count) {
+    const uint32_t seg_end = lv.seg_hi ? lv.seg_hi : count;
+    if (threadIdx.x == 0 && lv.seg_lo + blockIdx.x + lv.pf_stride < seg_end) {
         uint64_t po;
         int pv;
-        segment_of<MODE>(lv, blockIdx.x + lv.pf_stride, po, pv);
+        segment_of<MODE>(lv, lv.seg_lo + blockIdx.x + lv.pf_stride, po, pv);
         if (pv > 0 && (uint32_t)pv > lv.seg_min && (uint32_t)pv <= lv.seg_max) {   // this launch's
             prefetch_l2(reinterpret_cast<const KeyT*>(src) + po, (size_t)pv * sizeof(KeyT));
             if (KIND == KIND_PAIRS) prefetch_l2(src_v + po, (size_t)pv * 4);
@@ -1067,7 +1071,7 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK <= 512 ? 2 : 1)) k_segment_sort(
     }
     uint64_t off;
     int v;
-    segment_of<MODE>(lv, blockIdx.x, off, v);
+    segment_of<MODE>(lv, lv.seg_lo + blockIdx.x, off, v);
     if (v <= 0 || (uint32_t)v <= lv.seg_min || (uint32_t)v > lv.seg_max) return;
     A::run(src, src_v, off, v, lv.out, lv.out_v, smem_raw);
 }

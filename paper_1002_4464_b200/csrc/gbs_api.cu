@@ -90,6 +90,10 @@ constexpr uint32_t SMALL_TILE = 2048;      // small CTA configuration
 #endif
 constexpr bool GBS_SPLIT_STEP9_ON = GBS_SPLIT_STEP9;
 constexpr uint64_t SMALL_U64_TOTAL = 1u << 18;   // u64 levels up to this many samples use 2K tiles
+#ifndef GBS_U64_MED_TOTAL
+#define GBS_U64_MED_TOTAL 0                       // ... and up to this many 8K tiles (0 = off)
+#endif
+constexpr uint32_t MED_TILE_U64 = 8192;
 constexpr uint32_t D_MIN = 8;              // single level needs d >= 8
 constexpr uint32_t D_NEST = 32;            // d of a level with a nested Step 9
 constexpr uint32_t MAX_S = 4096;           // shared-memory limit of Steps 6 and 8
@@ -211,6 +215,13 @@ static int build_node(Plan& P, int kind, uint32_t B, uint64_t N, uint32_t pad_ba
         }
         if (s) {
             L = SMALL_TILE;
+        } else if (kind == KIND_U64 && (uint64_t)B * N <= GBS_U64_MED_TOTAL) {
+            // mid-size u64 level: half tiles (twice the CTAs) when one level with d >= D_MIN fits
+            for (uint32_t c = 2; c <= MED_TILE_U64 / D_MIN; c *= 2)
+                if (hi_bound(N, MED_TILE_U64, c) <= MED_TILE_U64) { s = c; break; }
+            if (s) L = MED_TILE_U64;
+        }
+        if (s) {
         } else {
             L = tile;
             for (uint32_t c = 2; c <= L / D_MIN; c *= 2)
@@ -356,7 +367,10 @@ static void launch_local(const LevelDev& lv, bool small, cudaStream_t st)
 {
     if (small) launch_local_t<KIND, GBS_SMALL>(lv, st);
     else if constexpr (KIND == KIND_KEYS) launch_local_t<KIND, GBS_BIG_KEYS>(lv, st);
-    else launch_local_t<KIND, GBS_BIG_WIDE>(lv, st);
+    else if constexpr (KIND == KIND_U64 && GBS_U64_MED_TOTAL > 0) {
+        if (lv.L == MED_TILE_U64) launch_local_t<KIND, 512, 16>(lv, st);
+        else launch_local_t<KIND, GBS_BIG_WIDE>(lv, st);
+    } else launch_local_t<KIND, GBS_BIG_WIDE>(lv, st);
 }
 
 template <int KIND, int MODE>

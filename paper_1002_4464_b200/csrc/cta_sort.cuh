@@ -201,6 +201,53 @@ struct CtaSort {
         }
     }
 
+    // The thread's ITEMS outputs [start, start+ITEMS) of the merge of two sorted runs of
+    // arbitrary lengths that fill the tile: run 1 = [0, len1), run 2 = [len1, TILE)
+    // (ties: run 1 first).  The final, cross-CTA level of a CTA-pair sort.
+    template <int M>
+    static __device__ __forceinline__ void merge_two(T (&x)[M], const T* sm, int start, int len1)
+    {
+        static_assert(M >= ITEMS, "register array too small");
+        const int len2 = TILE - len1;
+        int lo = max(0, start - len2), hi = min(start, len1);
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (sm[phys(mid)] <= sm[phys(len1 + start - 1 - mid)]) lo = mid + 1;
+            else hi = mid;
+        }
+        int ai = lo, bi = len1 + start - lo;
+        T a = ai < len1 ? sm[phys(ai)] : TMAX;
+        T b = bi < TILE ? sm[phys(bi)] : TMAX;
+        // warp-uniform fast path: no lane can exhaust a run within its ITEMS outputs
+        if (__all_sync(__activemask(), ai + ITEMS <= len1 && bi + ITEMS <= TILE)) {
+            const int cb = len1 + start + 1;             // bi after k steps = cb + k - ai
+#pragma unroll
+            for (int k = 0; k < ITEMS; ++k) {
+                const bool t = a <= b;
+                x[k] = t ? a : b;
+                ai += t ? 1 : 0;
+                const int nidx = t ? ai : cb + k - ai;
+                const T v = sm[phys_fma(nidx)];
+                a = t ? v : a;
+                b = t ? b : v;
+            }
+            return;
+        }
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k) {
+            const bool t = a <= b;
+            x[k] = t ? a : b;
+            ai += t ? 1 : 0;
+            bi += t ? 0 : 1;
+            const int nidx = t ? ai : bi;
+            const bool ok = nidx < (t ? len1 : TILE);
+            T v = sm[phys(ok ? nidx : 0)];
+            v = ok ? v : TMAX;
+            a = t ? v : a;
+            b = t ? b : v;
+        }
+    }
+
     // Tile whose runs of length R (power of two >= ITEMS) are already sorted: load it
     // into shared memory (phys layout, TMAX beyond valid) and run only the merge levels
     // w = R, 2R, ... .  Used for Step 4, whose input is m sorted runs of s samples

@@ -90,6 +90,9 @@ constexpr uint32_t SMALL_TILE = 2048;      // small CTA configuration
 #endif
 constexpr bool GBS_SPLIT_STEP9_ON = GBS_SPLIT_STEP9;
 constexpr uint64_t SMALL_U64_TOTAL = 1u << 18;   // u64 levels up to this many samples use 2K tiles
+#ifndef GBS_PAIR_BELOW_D
+#define GBS_PAIR_BELOW_D 16                       // CTA-pair sublists when the one-tile d is below (0 = off)
+#endif
 #ifndef GBS_U64_MED_TOTAL
 #define GBS_U64_MED_TOTAL 0                       // ... and up to this many 8K tiles (0 = off)
 #endif
@@ -118,6 +121,7 @@ struct Node {
     uint64_t Np = 0, hi = 0;
     uint32_t pad_base = 0;
     bool local_small = false, bucket_small = false;
+    bool local_pair = false;   // Step 2 on CTA pairs (L = 2 tiles, keys)
     int step4 = -1, step9 = -1;
     size_t o_samples = 0, o_splitters = 0, o_a = 0, o_l = 0, o_state = 0;
     size_t o_child_off = 0, o_child_len = 0, o_reloc = SIZE_MAX, o_reloc_v = SIZE_MAX;
@@ -226,6 +230,13 @@ static int build_node(Plan& P, int kind, uint32_t B, uint64_t N, uint32_t pad_ba
             L = tile;
             for (uint32_t c = 2; c <= L / D_MIN; c *= 2)
                 if (hi_bound(N, L, c) <= tile) { s = c; break; }
+            // keys whose one-tile plan needs d < GBS_PAIR_BELOW_D (samples > n/16): sublists
+            // of two tiles sorted by CTA pairs (NEXT-2) when that gives a one-level plan
+            // -- half the samples (Step 4) and twice the run length (Step 8) at equal bound
+            if (kind == KIND_KEYS && GBS_PAIR_BELOW_D > 0 && s && L / s < GBS_PAIR_BELOW_D) {
+                for (uint32_t c = 2; c <= 2 * tile / D_MIN; c *= 2)
+                    if (hi_bound(N, 2 * tile, c) <= tile) { L = 2 * tile; s = c; break; }
+            }
             if (!s) s = L / D_NEST;
         }
     }
@@ -238,6 +249,7 @@ static int build_node(Plan& P, int kind, uint32_t B, uint64_t N, uint32_t pad_ba
     if (nd.Np >= (1ull << 32) - (1ull << 20)) { snprintf(g_err, sizeof g_err, "problem too large for 32-bit tags"); return -1; }
     if (kind == KIND_U64 && (uint64_t)pad_base + nd.Np >= (1ull << 32)) { snprintf(g_err, sizeof g_err, "sentinel tag overflow"); return -1; }
     nd.local_small = L <= SMALL_TILE;
+    nd.local_pair = kind == KIND_KEYS && L == 2 * tile;
     const uint64_t ms = (uint64_t)B * nd.m * s;
     nd.o_samples = P.alloc(ms * 8);
     nd.o_splitters = P.alloc((uint64_t)B * s * 8);
@@ -292,9 +304,11 @@ static gbs_status_t make_plan(size_t n, int kind, const gbs_config_t* cfg, Plan&
     if (n > (1ull << 31)) return fail(GBS_ERROR_UNSUPPORTED, "n = %zu > 2^31", n);
     if (cfg && (cfg->L || cfg->s)) {
         const uint32_t L = cfg->L, s = cfg->s;
-        if (!pow2(L) || !pow2(s) || s > L || L > tile_of(kind) || s > MAX_S)
+        // keys may use sublists of two tiles (CTA-pair local sort); Step 9 stays one tile
+        const uint32_t maxL = kind == KIND_KEYS ? 2 * tile_of(kind) : tile_of(kind);
+        if (!pow2(L) || !pow2(s) || s > L || L > maxL || s > MAX_S || (L > tile_of(kind) && s < 2))
             return fail(GBS_ERROR_INVALID_VALUE, "bad config L=%u s=%u (powers of two, s<=L<=%u, s<=%u)", L, s,
-                        tile_of(kind), MAX_S);
+                        maxL, MAX_S);
     }
     P = Plan();
     if (n <= 1) return GBS_SUCCESS;
@@ -362,6 +376,17 @@ static void launch_seg_t(const LevelDev& lv, unsigned count, cudaStream_t st)
 }
 
 
+// Step 2 on CTA pairs: persistent clusters of two (one CTA per SM)
+static void launch_local_pair(const LevelDev& lv, cudaStream_t st)
+{
+    constexpr int BLOCK = GBS_KEYS_BLOCK, ITEMS = GBS_KEYS_ITEMS;
+    const size_t sm = Seg<KIND_KEYS, BLOCK, ITEMS>::smem_bytes();
+    static std::once_flag f;
+    std::call_once(f, [&] { set_smem(k_local_sort_pair<BLOCK, ITEMS>, sm); });
+    const unsigned pairs = std::min<unsigned>(lv.B * lv.m, num_sms() / 2);
+    k_local_sort_pair<BLOCK, ITEMS><<<2 * pairs, BLOCK, sm, st>>>(lv);
+}
+
 template <int KIND>
 static void launch_local(const LevelDev& lv, bool small, cudaStream_t st)
 {
@@ -386,7 +411,7 @@ static void launch_index(const LevelDev& lv, cudaStream_t st)
 {
     const size_t kb = key_bytes(KIND);
     // streaming TMA form when every chunk start is 16-byte aligned (contiguous problems)
-    const bool tma = GBS_IDX_TMA && lv.pr.off == nullptr && ((uintptr_t)lv.in & 15) == 0 &&
+    const bool tma = GBS_IDX_TMA && lv.pr.off == nullptr && ((uintptr_t)lv.srt & 15) == 0 &&
                      (lv.pr.stride * kb) % 16 == 0 && ((size_t)lv.L * kb) % 16 == 0 && lv.s <= 8 * IDX_BLOCK;
     if (tma) {
         const size_t sm = 2 * (size_t)IDX_CHUNK_BYTES + (size_t)lv.s * 12;
@@ -621,11 +646,13 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
             LevelDev lc = lv;
             lc.tile_lo = t0;
             lc.tile_hi = t1;
-            launch_local<KIND>(lc, nd.local_small, st);
+            if (nd.local_pair) launch_local_pair(lc, st);
+            else launch_local<KIND>(lc, nd.local_small, st);
             GBS_LAUNCHED();
         }
     } else {
-        launch_local<KIND>(lv, nd.local_small, st);
+        if (nd.local_pair) launch_local_pair(lv, st);
+        else launch_local<KIND>(lv, nd.local_small, st);
         GBS_LAUNCHED();
     }
     if (stop == 2 || stop == 3) return GBS_SUCCESS;

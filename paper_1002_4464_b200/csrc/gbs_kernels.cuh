@@ -17,6 +17,8 @@
 
 #include <type_traits>
 
+#include <cooperative_groups.h>
+
 #include "cta_sort.cuh"
 
 namespace gbs {
@@ -411,6 +413,126 @@ __global__ void __launch_bounds__(BLOCK, 1) k_local_sort(LevelDev lv)
         __syncthreads();                     // shared memory is reused by the next sublist
         start = nstart;
         v = nv;
+    }
+}
+
+// ------------------------------------------------------------ Steps 2 + 3 on a CTA pair
+// SURVEY NEXT-2 (the B200 reading of "n/m is the shared memory size"): a
+// sublist of L = 2 tiles is sorted by a thread-block cluster of two CTAs.  Each CTA sorts
+// its half on chip (CtaSort), then the last merge level crosses the pair through
+// distributed shared memory: with a* = the number of half-0 items among the first TILE
+// outputs (one merge-path split, found by a warp with 32-way probes of both halves),
+// CTA 0 outputs merge(A[0, a*), B[0, b*)) and CTA 1 merge(A[a*, T), B[b*, T)), b* = T - a*.
+// The two CTAs swap exactly b* items (CTA 0's A[a*, T) against CTA 1's B[0, b*), read
+// once over DSMEM), so each then holds its two runs in its own shared memory and runs
+// an ordinary uneven merge.  Samples (Step 3) at sublist positions (k+1)d - 1 come from
+// the CTA that outputs them.  Keys only.
+template <int BLOCK, int ITEMS>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BLOCK, 1) k_local_sort_pair(LevelDev lv)
+{
+    namespace cg = cooperative_groups;
+    using S = Seg<KIND_KEYS, BLOCK, ITEMS>;
+    using CS = typename S::CS;
+    using T = uint32_t;
+    constexpr int H = CS::TILE;                         // items per CTA (half a sublist)
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* sm = reinterpret_cast<T*>(smem_raw);
+    __shared__ int s_astar;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int rank = (int)cluster.block_rank();
+    const uint32_t ntiles = lv.tile_hi ? lv.tile_hi : lv.B * lv.m;
+    const uint32_t ncl = gridDim.x / 2;
+    T x[ITEMS];
+    bool have = false;                                  // x already holds this sublist's half
+    for (uint32_t tile = lv.tile_lo + blockIdx.x / 2; tile < ntiles; tile += ncl) {   // uniform in the pair
+        uint64_t start = 0;
+        int v = 0;
+        sublist_of(lv, tile, start, v);
+        const int vr = max(0, min(v - rank * H, H));
+        if (threadIdx.x == 0 && tile + ncl < ntiles) {
+            uint64_t ns;
+            int nv;
+            sublist_of(lv, tile + ncl, ns, nv);
+            const int nr = max(0, min(nv - rank * H, H));
+            if (nr > 0) prefetch_l2(reinterpret_cast<const T*>(lv.in) + ns + (uint64_t)rank * H, (size_t)nr * 4);
+        }
+        if (!have) S::load_regs(x, lv.in, nullptr, start + (uint64_t)rank * H, vr, smem_raw);
+        CS::sort(x, sm, vr);                            // positions >= vr read as TMAX
+        cluster.sync();                                 // both halves sorted and visible
+        const T* peer = cluster.map_shared_rank(sm, rank ^ 1);
+        if (threadIdx.x < 32) {
+            const T* A = rank == 0 ? sm : peer;         // half 0's sorted tile
+            const T* B = rank == 0 ? peer : sm;         // half 1's
+            // a* = first i in [0, H) with A[i] > B[H-1-i] (H if none): the merge-path
+            // split of diagonal H.  Invariant: the predicate is false below lo and true
+            // from hi on; each round probes 32 evenly spaced points (2 DSMEM-or-local
+            // reads per lane) and shrinks [lo, hi] 32-fold.
+            const int lane = threadIdx.x;
+            int lo = 0, hi = H;
+            while (lo < hi) {
+                const int step = (hi - lo + 31) / 32;
+                const int i = lo + lane * step;
+                const bool gt = i >= hi || A[CS::phys(i)] > B[CS::phys(H - 1 - i)];
+                const unsigned m = __ballot_sync(0xffffffffu, gt);
+                if (m == 0) {
+                    lo = lo + 31 * step + 1;
+                } else {
+                    const int f = __ffs(m) - 1;
+                    if (f == 0) hi = lo;
+                    else {
+                        hi = min(hi, lo + f * step);
+                        lo = lo + (f - 1) * step + 1;
+                    }
+                }
+            }
+            if (lane == 0) s_astar = lo;
+        }
+        __syncthreads();
+        const int astar = s_astar, bstar = H - astar;
+        // swap b* items: CTA 0 fetches B[0, b*), CTA 1 fetches A[a*, H).  Item q + k BLOCK
+        // sits at phys(q) + k (BLOCK + BLOCK/32): one base address, constant offsets.
+        static_assert(BLOCK % 32 == 0 && CS::PAD == 5, "swap addressing assumes one pad per 32");
+        constexpr int KSTEP = BLOCK + BLOCK / 32;
+        {
+            const int q = (int)threadIdx.x;
+            const T* src = peer + CS::phys((rank == 0 ? 0 : astar) + q);
+#pragma unroll
+            for (int k = 0; k < ITEMS; ++k) x[k] = q + k * BLOCK < bstar ? src[k * KSTEP] : T(0);
+            cluster.sync();                             // every remote read done
+            T* dst = sm + CS::phys((rank == 0 ? astar : 0) + q);
+#pragma unroll
+            for (int k = 0; k < ITEMS; ++k)
+                if (q + k * BLOCK < bstar) dst[k * KSTEP] = x[k];
+        }
+        __syncthreads();
+        // local runs: rank 0 [A[0,a*) | B[0,b*)], rank 1 [A[a*,H) | B[b*,H)]; A part first
+        const int len1 = rank == 0 ? astar : bstar;
+        CS::merge_two(x, sm, (int)threadIdx.x * ITEMS, len1);
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k) sm[CS::phys((int)threadIdx.x * ITEMS + k)] = x[k];
+        __syncthreads();
+        // the next sublist's half is loaded into the free registers now, in flight
+        // during the write-back (software pipelining, as k_local_sort)
+        have = tile + ncl < ntiles;
+        if (have) {
+            uint64_t nstart;
+            int nv;
+            sublist_of(lv, tile + ncl, nstart, nv);
+            S::load_regs(x, lv.in, nullptr, nstart + (uint64_t)rank * H, max(0, min(nv - rank * H, H)), smem_raw);
+        }
+        if (vr > 0) S::store(lv.srt, nullptr, start + (uint64_t)rank * H, vr, smem_raw);
+        // Step 3: samples k whose position (k+1)d - 1 falls in this CTA's half
+        const uint32_t i = tile % lv.m, b = tile / lv.m;
+        const uint64_t i0 = (uint64_t)i * lv.L;
+        u64* smp = lv.samples + ((uint64_t)b * lv.m + i) * lv.s;
+        const uint32_t k0 = (uint32_t)rank * (lv.s / 2), k1 = k0 + lv.s / 2;
+        for (uint32_t k = k0 + threadIdx.x; k < k1; k += BLOCK) {
+            const uint32_t r = (k + 1) * lv.d - 1;
+            const uint32_t key = (int)r < v ? sm[CS::phys((int)r - rank * H)] : 0xFFFFFFFFu;
+            smp[k] = ((unsigned long long)key << 32) | (uint32_t)(i0 + r);
+        }
+        __syncthreads();                                // shared memory reused next sublist
     }
 }
 

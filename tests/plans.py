@@ -12,6 +12,7 @@ TILE_KEYS = 1 << 15     # u32 keys per CTA tile (128 KB of shared memory)
 TILE_PAIRS = 1 << 14    # (key, value) pairs per CTA tile
 D_MIN = 8               # a single level needs d = L/s >= 8 (samples <= n/8)
 D_NEST = 32             # d of a level whose buckets need a nested level
+PAIR_BELOW_D = 16       # keys: sublists of two tiles (CTA pairs) when the one-tile d is below
 
 
 def hi_bound(cap: int, L: int, s: int) -> int:
@@ -36,6 +37,15 @@ def plan(n: int, tile: int = TILE_KEYS, cfg=None):
                 chosen = s
                 break
             s *= 2
+        # keys: if the one-tile level needs d < 16, sublists of two tiles (sorted by a
+        # CTA pair) with buckets still one tile, when that is one level too
+        if tile == TILE_KEYS and chosen is not None and L // chosen < PAIR_BELOW_D:
+            s = 2
+            while s <= 2 * tile // D_MIN:
+                if hi_bound(cap, 2 * tile, s) <= tile:
+                    L, chosen = 2 * tile, s
+                    break
+                s *= 2
         if chosen is not None:
             levels.append((L, chosen))
             break

@@ -41,7 +41,8 @@ def gpu_sort(keys, dev, vals=None, cfg=None, stop=0, ws=None):
     return to_np(k), (to_np(v) if v is not None else None)
 
 
-SIZES = [0, 1, 2, 3, 31, 1023, 2048, 2049, 32768, 32769, 65536, 100003, 1 << 20, 3 * (1 << 20) + 17]
+SIZES = [0, 1, 2, 3, 31, 1023, 2048, 2049, 32768, 32769, 65536, 100003, 1 << 20, 3 * (1 << 20) + 17,
+         (1 << 22) + 12345]
 
 
 @pytest.mark.parametrize("n", SIZES)
@@ -50,6 +51,18 @@ def test_keys_default_plan(dev, n, dist):
     keys = gi.generate(dist, n, seed=n % 5)
     got, _ = gpu_sort(keys, dev)
     exp, _, _ = oracle.gbs_sort(keys, plan=plan(n, TILE_KEYS))
+    assert np.array_equal(got, exp)
+
+
+@pytest.mark.parametrize("n,cfg", [((1 << 22) + 12345, (1 << 16, 256)), (5_000_003, (1 << 16, 1024)),
+                                   (70_000, (1 << 16, 16))])
+@pytest.mark.parametrize("dist", gi.DISTRIBUTIONS)
+def test_keys_cta_pair_plan(dev, n, cfg, dist):
+    """Sublists of two tiles sorted by a CTA pair (NEXT-2): ragged last sublists whose
+    second half is empty or partial."""
+    keys = gi.generate(dist, n, seed=n % 5)
+    got, _ = gpu_sort(keys, dev, cfg=cfg)
+    exp, _, _ = oracle.gbs_sort(keys, plan=plan(n, TILE_KEYS, cfg))
     assert np.array_equal(got, exp)
 
 
@@ -65,7 +78,8 @@ def test_keys_C1_paper_plan(dev, seed, dist):
 
 
 @pytest.mark.parametrize("cfg,n", [((2048, 64), 1 << 16), (None, 1 << 16), (None, 3 * (1 << 20) + 17),
-                                   ((4096, 256), 500_000), ((1024, 32), 300_001)])
+                                   ((4096, 256), 500_000), ((1024, 32), 300_001),
+                                   ((1 << 16, 512), 3_000_017), ((1 << 16, 64), 100_000)])
 @pytest.mark.parametrize("dist", ["uniform", "zero", "det_duplicates", "staggered"])
 def test_stage_parity(dev, cfg, n, dist):
     """Every level-1 intermediate equals the oracle's: sorted sublists (Step 2), samples

@@ -67,9 +67,13 @@ def test_validation_before_device_work():
     # NULL keys with n > 1 -> INVALID_VALUE (rejected before any device query)
     assert L.gbs_sort_keys(None, 10, None, 0, None) == 1
     # bad configs
-    for cfg in [(3000, 64), (2048, 4096), (1 << 16, 64), (64, 128)]:
+    for cfg in [(3000, 64), (2048, 4096), (1 << 17, 64), (64, 128)]:
         with pytest.raises(gbs.GbsError):
             gbs.plan(1 << 16, cfg=cfg)
+    # sublists of two tiles (CTA-pair local sort) are keys-only
+    assert gbs.plan(1 << 20, cfg=(1 << 16, 64))["levels"][0] == (1 << 16, 64)
+    with pytest.raises(gbs.GbsError):
+        gbs.plan(1 << 20, pairs=True, cfg=(1 << 15, 64))
     with pytest.raises(gbs.GbsError):
         gbs.plan((1 << 31) + 1)
     # workspace too small is reported, not crashed on

@@ -245,7 +245,11 @@ def test_plan_rule_table_P():
     """DESIGN.md section 5 plans for the five configs."""
     assert plan(1 << 16, cfg=(2048, 64)) == [(2048, 64)]
     assert plan(1 << 25) == [(TILE_KEYS, 2048)] and hi_bound(1 << 25, TILE_KEYS, 2048) == 31729
-    assert plan(1 << 26) == [(TILE_KEYS, 4096)] and hi_bound(1 << 26, TILE_KEYS, 4096) == 30713
+    # one tile would need d = 8 here: sublists of two tiles (CTA pairs), buckets one tile
+    assert plan(1 << 26) == [(2 * TILE_KEYS, 4096)] and hi_bound(1 << 26, 2 * TILE_KEYS, 4096) == 31729
+    assert hi_bound(1 << 26, TILE_KEYS, 4096) == 30713
+    assert plan(3 << 24) == [(2 * TILE_KEYS, 4096)] and plan((1 << 25) + 1) == [(TILE_KEYS, 2048)]
+    assert all(hi_bound(n, *plan(n)[0]) <= TILE_KEYS for n in (1 << 22, 3 << 24, 1 << 26))
     assert plan(1 << 30, TILE_PAIRS) == [(TILE_PAIRS, 512), (TILE_PAIRS, 512)]
     assert hi_bound(1 << 30, TILE_PAIRS, 512) == 4128737
     assert hi_bound(4128737, TILE_PAIRS, 512) == 15845

@@ -416,6 +416,9 @@ __global__ void __launch_bounds__(BLOCK, 1) k_local_sort(LevelDev lv)
     }
 }
 
+#ifndef GBS_PAIR_PREFETCH
+#define GBS_PAIR_PREFETCH 0   // CTA-pair local sort: next half into registers during the write-back (measured slower: spills)
+#endif
 // ------------------------------------------------------------ Steps 2 + 3 on a CTA pair
 // SURVEY NEXT-2 (the B200 reading of "n/m is the shared memory size"): a
 // sublist of L = 2 tiles is sorted by a thread-block cluster of two CTAs.  Each CTA sorts
@@ -514,7 +517,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BLOCK, 1) k_local_so
         __syncthreads();
         // the next sublist's half is loaded into the free registers now, in flight
         // during the write-back (software pipelining, as k_local_sort)
-        have = tile + ncl < ntiles;
+        have = GBS_PAIR_PREFETCH && tile + ncl < ntiles;
         if (have) {
             uint64_t nstart;
             int nv;

@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--dist", default="uniform")
     ap.add_argument("--impl", default="gbs", choices=["gbs", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer leg (profiling runs only)")
     ap.add_argument("--n", type=int, default=0, help="override the workload's size (experiments; not a bench line)")
     ap.add_argument("--force-dist", action="store_true",
                     help="use the multi-GPU entry even with one rank (exercises E1-E9 on one GPU)")
@@ -312,8 +313,6 @@ def main():
     if use_dist:
         dist.barrier()
     torch.cuda.synchronize()
-    if comm is None:
-        gbs.profile_begin()
     with ClockSampler(local) as clk:
         for i in range(args.steps):
             restore()
@@ -322,7 +321,19 @@ def main():
             one_sort()
             ends[i].record(stream)
         torch.cuda.synchronize()
-    prof = gbs.profile_end() if comm is None else None
+    # Per-step kernel times (roofline, breakdown): a second timed pass of the same steps
+    # with the library's per-step CUDA events on the call's stream.  Kept out of the
+    # headline pass: an event between two kernels stops the programmatic dependent
+    # launch at that boundary (~1-2 % per step).
+    prof = None
+    if comm is None:
+        gbs.profile_begin()
+        for i in range(min(args.steps, 10)):
+            restore()
+            flush.zero_()
+            one_sort()
+        torch.cuda.synchronize()
+        prof = gbs.profile_end()
     if use_dist:
         dist.barrier()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
@@ -336,7 +347,7 @@ def main():
 
     # ---- end to end through the C-ABI with host buffers (N = 1)
     e2e = None
-    if comm is None and not pairs:
+    if comm is None and not pairs and not args.no_e2e:
         host = pristine.cpu().pin_memory()
         hbuf = torch.empty_like(host).pin_memory()
         dbuf = torch.empty_like(keys)

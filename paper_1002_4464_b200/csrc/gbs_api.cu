@@ -94,7 +94,7 @@ constexpr uint64_t SMALL_U64_TOTAL = 1u << 18;   // u64 levels up to this many s
 #define GBS_PAIR_BELOW_D 16                       // CTA-pair sublists when the one-tile d is below (0 = off)
 #endif
 #ifndef GBS_U64_MED_TOTAL
-#define GBS_U64_MED_TOTAL 0                       // ... and up to this many 8K tiles (0 = off)
+#define GBS_U64_MED_TOTAL 0                       // ... and up to this many 8K tiles (0 = off; measured slower at C2/C3)
 #endif
 constexpr uint32_t MED_TILE_U64 = 8192;
 constexpr uint32_t D_MIN = 8;              // single level needs d >= 8
@@ -332,6 +332,29 @@ static uint32_t num_sms();
 #define GBS_IDX_TMA 1
 #endif
 
+#ifndef GBS_PDL
+#define GBS_PDL 1   // programmatic dependent launch between the kernels of a sort
+#endif
+// <<<grid, block, smem, st>>> with the programmatic-stream-serialization attribute: the
+// kernel may launch while its predecessor on the stream drains (each kernel waits on
+// griddepcontrol.wait before touching global memory; pdl_entry in gbs_kernels.cuh).
+template <typename... KArgs, typename... Args>
+static void launch_k(void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
+                     Args&&... args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = GBS_PDL;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 template <typename K>
 static void set_smem(K kernel, size_t bytes)
 {
@@ -352,7 +375,7 @@ static void launch_local_t(const LevelDev& lv0, cudaStream_t st)
     });
     // persistent: one CTA per resident slot, each walks tiles blockIdx.x + k*gridDim.x
     const unsigned grid = std::min<unsigned>(lv0.B * lv0.m, num_sms() * (unsigned)occ);
-    k_local_sort<KIND, BLOCK, ITEMS><<<grid, BLOCK, sm, st>>>(lv0);
+    launch_k(k_local_sort<KIND, BLOCK, ITEMS>, grid, BLOCK, sm, st, lv0);
 }
 
 template <int KIND, int BLOCK, int ITEMS, int MODE>
@@ -372,7 +395,7 @@ static void launch_seg_t(const LevelDev& lv, unsigned count, cudaStream_t st)
     });
     (void)occ;
     // one CTA per segment (for a size tier: per list slot, the unused tail exits at once)
-    k_segment_sort<KIND, BLOCK, ITEMS, MODE><<<count, BLOCK, sm, st>>>(lv);
+    launch_k(k_segment_sort<KIND, BLOCK, ITEMS, MODE>, count, BLOCK, sm, st, lv);
 }
 
 
@@ -384,7 +407,7 @@ static void launch_local_pair(const LevelDev& lv, cudaStream_t st)
     static std::once_flag f;
     std::call_once(f, [&] { set_smem(k_local_sort_pair<BLOCK, ITEMS>, sm); });
     const unsigned pairs = std::min<unsigned>(lv.B * lv.m, num_sms() / 2);
-    k_local_sort_pair<BLOCK, ITEMS><<<2 * pairs, BLOCK, sm, st>>>(lv);
+    launch_k(k_local_sort_pair<BLOCK, ITEMS>, 2 * pairs, BLOCK, sm, st, lv);
 }
 
 template <int KIND>
@@ -418,14 +441,14 @@ static void launch_index(const LevelDev& lv, cudaStream_t st)
         static std::once_flag f2;
         std::call_once(f2, [&] { set_smem(k_sample_index_tma<KIND, IDX_BLOCK, 8>, 220 * 1024); });
         const unsigned grid = std::min<unsigned>(lv.B * lv.m, num_sms());
-        k_sample_index_tma<KIND, IDX_BLOCK, 8><<<grid, IDX_BLOCK, sm, st>>>(lv);
+        launch_k(k_sample_index_tma<KIND, IDX_BLOCK, 8>, grid, IDX_BLOCK, sm, st, lv);
         return;
     }
     const size_t chunk = std::min<size_t>((size_t)lv.L * key_bytes(KIND), IDX_CHUNK_BYTES);
     const size_t sm = (size_t)lv.s * 8 + (size_t)(lv.s + (lv.s & 1)) * 4 + chunk;
     static std::once_flag f;
     std::call_once(f, [&] { set_smem(k_sample_index<KIND, IDX_BLOCK>, 227 * 1024); });
-    k_sample_index<KIND, IDX_BLOCK><<<lv.B * lv.m, IDX_BLOCK, sm, st>>>(lv);
+    launch_k(k_sample_index<KIND, IDX_BLOCK>, lv.B * lv.m, IDX_BLOCK, sm, st, lv);
 }
 
 template <int KIND>
@@ -436,7 +459,7 @@ static void launch_relocate(const LevelDev& lv, cudaStream_t st)
     const size_t sm = (size_t)2 * lv.s * 4 + (lv.L + 2 * (lv.L / per) + 4) * 2;
     static std::once_flag f;
     std::call_once(f, [&] { set_smem(k_relocate<KIND, IDX_BLOCK, MAXPER>, 220 * 1024); });
-    k_relocate<KIND, IDX_BLOCK, MAXPER><<<lv.B * lv.m, IDX_BLOCK, sm, st>>>(lv);
+    launch_k(k_relocate<KIND, IDX_BLOCK, MAXPER>, lv.B * lv.m, IDX_BLOCK, sm, st, lv);
 }
 
 static uint32_t num_sms()
@@ -519,7 +542,7 @@ static gbs_status_t launch_step9(const LevelDev& lv, const Node& nd, char* ws, c
             uint32_t* lens = lists + 3 * (uint64_t)count;
             const uint32_t cut1 = GBS_MID_STEP9 ? mid_cap(KIND) : TILE;
             GBS_CUDA(cudaMemsetAsync(lens, 0, 16, st));
-            k_bucket_tiers<<<(count + 255) / 256, 256, 0, st>>>(lv, lists, lens, TILE / 2, cut1);
+            launch_k(k_bucket_tiers, (count + 255) / 256, 256, 0, st, lv, lists, lens, TILE / 2, cut1);
             GBS_LAUNCHED();
             LevelDev t0 = lv, t1 = lv, t2 = lv;
             t0.tier_list = lists;
@@ -674,7 +697,7 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
     // runs only when a caller stops right after Step 5 (stage parity).
     if (stop == 5) {
         const uint64_t tot = (uint64_t)nd.B * nd.s;
-        k_global_samples<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(lv);
+        launch_k(k_global_samples, (unsigned)((tot + 255) / 256), 256, 0, st, lv);
         GBS_LAUNCHED();
         return GBS_SUCCESS;
     }
@@ -687,7 +710,7 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
         unsigned* dflag = nullptr;
         GBS_CUDA(cudaMallocManaged(&dflag, 8 * sizeof(unsigned)));
         memset(dflag, 0, 8 * sizeof(unsigned));
-        k_check_level<<<1024, 256, 0, st>>>(lv, dflag);
+        launch_k(k_check_level, 1024, 256, 0, st, lv, dflag);
         GBS_CUDA(cudaStreamSynchronize(st));
         unsigned fl[8];
         memcpy(fl, dflag, sizeof fl);
@@ -704,7 +727,7 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
     // Step 7: column-major exclusive scan -> l
     const unsigned nblk = (nd.s + 31) / 32;
     GBS_CUDA(cudaMemsetAsync(lv.state, 0, (size_t)nd.B * nblk * 8, st));
-    k_scan<<<nd.B * nblk, SCAN_BLOCK, 0, st>>>(lv);
+    launch_k(k_scan, nd.B * nblk, SCAN_BLOCK, 0, st, lv);
     GBS_LAUNCHED();
     if (stop == 7) return GBS_SUCCESS;
     pm.mark();
@@ -761,7 +784,7 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
         lv.child_off = reinterpret_cast<u64*>(ws + nd.o_child_off);
         lv.child_len = reinterpret_cast<uint32_t*>(ws + nd.o_child_len);
         const uint64_t tot = (uint64_t)nd.B * nd.s;
-        k_child_desc<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(lv);
+        launch_k(k_child_desc, (unsigned)((tot + 255) / 256), 256, 0, st, lv);
         GBS_LAUNCHED();
         Bufs b9{bf.reloc, bf.in, bf.out, bf.reloc_v, bf.in_v, bf.out_v};
         Probs p9{lv.child_off, lv.child_len, 0, 0};

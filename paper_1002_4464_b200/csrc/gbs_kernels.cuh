@@ -26,6 +26,17 @@ namespace gbs {
 typedef unsigned long long u64;
 __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
 
+// Programmatic dependent launch (sm_90+): every kernel of a sort lets its successor's
+// CTAs launch as soon as all of its own CTAs are resident, and waits for its
+// predecessor's completion (and memory) before touching global memory.  The successor
+// thus fills the SMs the predecessor's last wave frees instead of waiting for the
+// launch after the grid drains.  No-ops for a normal launch.
+__device__ __forceinline__ void pdl_entry()
+{
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 enum Kind { KIND_KEYS = 0, KIND_PAIRS = 1, KIND_U64 = 2 };
 
 struct Probs {
@@ -352,6 +363,7 @@ struct Adapt {
 template <int KIND, int BLOCK, int ITEMS>
 __global__ void __launch_bounds__(BLOCK, 1) k_local_sort(LevelDev lv)
 {
+    pdl_entry();
     using S = Seg<KIND, BLOCK, ITEMS>;
     using T = typename S::T;
     using KeyT = typename S::KeyT;
@@ -433,6 +445,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_local_sort(LevelDev lv)
 template <int BLOCK, int ITEMS>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BLOCK, 1) k_local_sort_pair(LevelDev lv)
 {
+    pdl_entry();
     namespace cg = cooperative_groups;
     using S = Seg<KIND_KEYS, BLOCK, ITEMS>;
     using CS = typename S::CS;
@@ -543,6 +556,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BLOCK, 1) k_local_so
 // Global sampling: g_k = sorted_samples[(k+1)m - 1] (R2).
 __global__ void k_global_samples(LevelDev lv)
 {
+    pdl_entry();
     const uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (uint64_t)lv.B * lv.s) return;
     const uint32_t b = (uint32_t)(idx / lv.s), k = (uint32_t)(idx % lv.s);
@@ -587,6 +601,7 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phas
 template <int KIND, int BLOCK, int MAXQ>
 __global__ void __launch_bounds__(BLOCK, 1) k_sample_index_tma(LevelDev lv)
 {
+    pdl_entry();
     using KT = typename std::conditional<KIND == KIND_U64, unsigned long long, uint32_t>::type;
     constexpr int CH = IDX_CHUNK_BYTES / sizeof(KT);
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -724,6 +739,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_sample_index_tma(LevelDev lv)
 template <int KIND, int BLOCK>
 __global__ void __launch_bounds__(BLOCK, 2) k_sample_index(LevelDev lv)
 {
+    pdl_entry();
     using KT = typename std::conditional<KIND == KIND_U64, unsigned long long, uint32_t>::type;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     unsigned long long* gs = reinterpret_cast<unsigned long long*>(smem_raw);
@@ -802,6 +818,7 @@ static constexpr unsigned long long LB_AGG = 1ull << 62, LB_INC = 2ull << 62, LB
 
 __global__ void __launch_bounds__(SCAN_BLOCK) k_scan(LevelDev lv)
 {
+    pdl_entry();
     constexpr int NW = SCAN_BLOCK / 32;
     __shared__ uint32_t wsum[NW][33];
     __shared__ uint32_t colpre[32];
@@ -933,6 +950,7 @@ __device__ __forceinline__ int upper_bound_u32(const uint32_t* a, int lo, int hi
 template <int KIND, int BLOCK, int MAXPER>
 __global__ void __launch_bounds__(BLOCK, 2) k_relocate(LevelDev lv)
 {
+    pdl_entry();
     using KT = typename std::conditional<KIND == KIND_U64, unsigned long long, uint32_t>::type;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint32_t* starts = reinterpret_cast<uint32_t*>(smem_raw);
@@ -1067,6 +1085,7 @@ __device__ __forceinline__ void segment_of(const LevelDev& lv, uint32_t idx, uin
 __global__ void __launch_bounds__(256) k_bucket_tiers(LevelDev lv, uint32_t* lists, uint32_t* lens, uint32_t cut0,
                                                       uint32_t cut1)
 {
+    pdl_entry();
     __shared__ uint32_t wcnt[3][8], wbase[3][8];
     const uint32_t count = lv.B * lv.s;
     const uint32_t idx = blockIdx.x * 256 + threadIdx.x;
@@ -1116,6 +1135,7 @@ __host__ __device__ constexpr uint32_t gather_max_m(int kind) { return kind == K
 template <int KIND, int BLOCK, int ITEMS, int MODE>
 __global__ void __launch_bounds__(BLOCK, (BLOCK <= 512 ? 2 : 1)) k_segment_sort(LevelDev lv)
 {
+    pdl_entry();
     // the mid tier (ITEMS not a power of two) only sees sizes just above the small tier
     using A = Adapt<KIND, BLOCK, ITEMS, ((ITEMS & (ITEMS - 1)) == 0 ? GBS_ADAPT_DEPTH : 0)>;
     using KeyT = typename A::S::KeyT;
@@ -1206,6 +1226,7 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK <= 512 ? 2 : 1)) k_segment_sort(
 // real item count (conservation).
 __global__ void k_check_level(LevelDev lv, unsigned* flag)
 {
+    pdl_entry();
     const uint64_t ms = (uint64_t)lv.m * lv.s;
     for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < (uint64_t)lv.B * ms;
          q += (uint64_t)gridDim.x * blockDim.x) {
@@ -1230,6 +1251,7 @@ __global__ void k_check_level(LevelDev lv, unsigned* flag)
 // Nested Step 9: the buckets of this level become the problems of the next level.
 __global__ void k_child_desc(LevelDev lv)
 {
+    pdl_entry();
     const uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= (uint64_t)lv.B * lv.s) return;
     const uint32_t b = (uint32_t)(idx / lv.s), j = (uint32_t)(idx % lv.s);

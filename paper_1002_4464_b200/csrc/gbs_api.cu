@@ -439,8 +439,16 @@ static void launch_index(const LevelDev& lv, cudaStream_t st)
     if (tma) {
         const size_t sm = 2 * (size_t)IDX_CHUNK_BYTES + (size_t)lv.s * 12;
         static std::once_flag f2;
-        std::call_once(f2, [&] { set_smem(k_sample_index_tma<KIND, IDX_BLOCK, 8>, 220 * 1024); });
-        const unsigned grid = std::min<unsigned>(lv.B * lv.m, num_sms());
+        static int occ = 1;
+        std::call_once(f2, [&] {
+            set_smem(k_sample_index_tma<KIND, IDX_BLOCK, 8>, 220 * 1024);
+            // occupancy at the largest table this kernel sees (s <= 4096)
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sample_index_tma<KIND, IDX_BLOCK, 8>, IDX_BLOCK,
+                                                              2 * (size_t)IDX_CHUNK_BYTES + 4096 * 12) != cudaSuccess ||
+                occ < 1)
+                occ = 1;
+        });
+        const unsigned grid = std::min<unsigned>(lv.B * lv.m, num_sms() * (unsigned)occ);
         launch_k(k_sample_index_tma<KIND, IDX_BLOCK, 8>, grid, IDX_BLOCK, sm, st, lv);
         return;
     }

@@ -570,7 +570,10 @@ __global__ void k_global_samples(LevelDev lv)
 // (the paper loads the s global samples into shared memory); each thread
 // bisects for its splitters -- the paper's staged schedule only avoided
 // GT200 bank contention and does not change the result (R10).
-static constexpr int IDX_CHUNK_BYTES = 64 * 1024;
+#ifndef GBS_IDX_CHUNK_KB
+#define GBS_IDX_CHUNK_KB 64
+#endif
+static constexpr int IDX_CHUNK_BYTES = GBS_IDX_CHUNK_KB * 1024;
 
 // --- TMA bulk copy + mbarrier helpers (sm_90+ PTX; SASS UBLKCP / SYNCS)
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -599,7 +602,7 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phas
 // threads bisect the current one.  Used when every chunk start is 16-byte aligned
 // (contiguous problems; the host checks); per-splitter counts accumulate in registers.
 template <int KIND, int BLOCK, int MAXQ>
-__global__ void __launch_bounds__(BLOCK, 1) k_sample_index_tma(LevelDev lv)
+__global__ void __launch_bounds__(BLOCK, (GBS_IDX_CHUNK_KB <= 32 ? 2 : 1)) k_sample_index_tma(LevelDev lv)
 {
     pdl_entry();
     using KT = typename std::conditional<KIND == KIND_U64, unsigned long long, uint32_t>::type;
@@ -813,7 +816,10 @@ __global__ void __launch_bounds__(BLOCK, 2) k_sample_index(LevelDev lv)
 // of 32 columns: pass 1 column sums (the paper's "parallel column sum"), one
 // decoupled look-back across column blocks replaces the single-SM scan of column
 // sums, pass 2 writes l (the paper's "final update").  Integer sums: deterministic.
-static constexpr int SCAN_BLOCK = 512;
+#ifndef GBS_SCAN_BLOCK
+#define GBS_SCAN_BLOCK 1024
+#endif
+static constexpr int SCAN_BLOCK = GBS_SCAN_BLOCK;
 static constexpr unsigned long long LB_AGG = 1ull << 62, LB_INC = 2ull << 62, LB_VAL = (1ull << 62) - 1;
 
 __global__ void __launch_bounds__(SCAN_BLOCK) k_scan(LevelDev lv)
@@ -836,10 +842,12 @@ __global__ void __launch_bounds__(SCAN_BLOCK) k_scan(LevelDev lv)
     uint32_t sum = 0;
     if (col_ok) {
         uint64_t r = r0;
-        for (; r + 4 <= r1; r += 4) {
-            const uint32_t x0 = A[(r + 0) * lv.s + c], x1 = A[(r + 1) * lv.s + c];
-            const uint32_t x2 = A[(r + 2) * lv.s + c], x3 = A[(r + 3) * lv.s + c];
-            sum += x0 + x1 + x2 + x3;
+        for (; r + 8 <= r1; r += 8) {           // 8 independent loads in flight
+            uint32_t x[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) x[u] = A[(r + u) * lv.s + c];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) sum += x[u];
         }
         for (; r < r1; ++r) sum += A[r * lv.s + c];
     }

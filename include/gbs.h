@@ -157,6 +157,17 @@ gbs_status_t gbs_sort_keys_dist(gbs_comm_t comm, uint32_t* d_keys, size_t n_loca
                                 uint32_t* d_out, size_t out_capacity, size_t* n_out, void* d_ws,
                                 size_t ws_bytes, gbs_stream_t stream);
 
+/* The p-rank path of gbs_sort_keys_dist on ONE GPU, for testing: the same per-rank
+ * phases (E1-E2, E4-E6, E9 kernels) run for ranks 0..p-1 in turn, and the collectives
+ * (E3, E7 allgathers, E8 all-to-all) are replaced by device copies.  d_keys holds the
+ * p shards back to back (p*n_local keys), d_out p regions of out_capacity keys (rank
+ * k's part at d_out + k*out_capacity), n_out a host array of p lengths, d_ws p
+ * workspaces of ws_bytes (per-rank size from gbs_sort_keys_dist_workspace_size).
+ * Synchronises `stream` once (E7). */
+gbs_status_t gbs_sort_keys_dist_emulated(int p, uint32_t* d_keys, size_t n_local, uint32_t* d_out,
+                                         size_t out_capacity, size_t* n_out, void* d_ws,
+                                         size_t ws_bytes, gbs_stream_t stream);
+
 /* Host-only exchange plan (E7-E8), exported so the protocol can be tested without a
  * GPU.  cuts: p x p row-major, cuts[r*p + k] = cut_{r,k} (#items of rank r's sorted
  * shard <= splitter k; cuts[r*p + p-1] = n_local).  For `rank`, fills send_off/

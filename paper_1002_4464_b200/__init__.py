@@ -74,6 +74,7 @@ def lib():
             "gbs_comm_destroy": [p],
             "gbs_sort_keys_dist_workspace_size": [sz, C.c_int, C.POINTER(sz), C.POINTER(sz)],
             "gbs_sort_keys_dist": [p, p, sz, p, sz, C.POINTER(sz), p, sz, p],
+            "gbs_sort_keys_dist_emulated": [C.c_int, p, sz, p, sz, p, p, sz, p],
             "gbs_exchange_plan": [p, C.c_int, C.c_int, p, p, p, p, p],
             "gbs_profile_begin": [],
             "gbs_profile_end": [C.POINTER(StepTimes)],
@@ -319,3 +320,21 @@ def sort_keys_dist(keys, comm: Comm, out=None, ws: Workspace | None = None, stre
     _check(lib().gbs_sort_keys_dist(comm.handle, C.c_void_p(kp), n, C.c_void_p(out.data_ptr()), out.numel(),
                                     C.byref(n_out), wp, wb, _stream(stream)))
     return out[:n_out.value]
+
+
+def sort_keys_dist_emulated(shards, p: int, stream=None):
+    """Testing aid: the p-rank multi-GPU path on one GPU (collectives replaced by device
+    copies).  ``shards``: p*n_local keys, rank r's shard at [r n_local, (r+1) n_local)
+    (sorted locally in place).  Returns the list of the p ranks' parts."""
+    torch = _torch()
+    assert shards.numel() % p == 0
+    n = shards.numel() // p
+    kp = _dev_ptr(shards, "shards")
+    need, cap = dist_workspace_size(n, p)
+    out = torch.empty(p * cap, dtype=shards.dtype, device=shards.device)
+    ws = torch.empty(p * need + 256, dtype=torch.uint8, device=shards.device)
+    wp = (ws.data_ptr() + 255) // 256 * 256
+    n_out = (C.c_size_t * p)()
+    _check(lib().gbs_sort_keys_dist_emulated(p, C.c_void_p(kp), n, C.c_void_p(out.data_ptr()), cap, n_out,
+                                             C.c_void_p(wp), need, _stream(stream)))
+    return [out[r * cap:r * cap + n_out[r]] for r in range(p)]

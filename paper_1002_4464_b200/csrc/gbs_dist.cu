@@ -210,6 +210,79 @@ gbs_status_t gbs_sort_keys_dist_workspace_size(size_t n_local, int nranks, size_
     return GBS_SUCCESS;
 }
 
+}  // extern "C"
+
+namespace {
+
+// One rank's view of E1-E9: the phases between the collectives, shared by the NCCL path
+// and the single-GPU emulation (gbs_sort_keys_dist_emulated).
+struct RankCtx {
+    uint32_t* keys;
+    uint32_t* out;
+    char* ws;
+    size_t n_local;
+    int p, rank;
+    uint32_t s_r;
+    DistLayout L;
+    unsigned long long *samples, *gathered, *cuts, *all_cuts;
+    cudaStream_t st;
+};
+
+gbs_status_t rank_ctx(RankCtx& c, uint32_t* keys, uint32_t* out, void* ws, size_t n_local, int p, int rank,
+                      cudaStream_t st)
+{
+    c.keys = keys;
+    c.out = out;
+    c.ws = reinterpret_cast<char*>(ws);
+    c.n_local = n_local;
+    c.p = p;
+    c.rank = rank;
+    c.s_r = s_r_of(n_local);
+    c.st = st;
+    gbs_status_t r = dist_layout(n_local, p, &c.L);
+    if (r) return r;
+    c.samples = reinterpret_cast<unsigned long long*>(c.ws + c.L.samples);
+    c.gathered = reinterpret_cast<unsigned long long*>(c.ws + c.L.gathered);
+    c.cuts = reinterpret_cast<unsigned long long*>(c.ws + c.L.cuts);
+    c.all_cuts = reinterpret_cast<unsigned long long*>(c.ws + c.L.all_cuts);
+    return GBS_SUCCESS;
+}
+
+// E1 local GBS of the shard, E2 regular samples (key, global position)
+gbs_status_t phase_local(const RankCtx& c)
+{
+    gbs_status_t r = gbs_sort_keys(c.keys, c.n_local, c.ws, c.L.samples, c.st);
+    if (r) return r;
+    const uint64_t gbase = (uint64_t)c.rank * c.n_local;
+    k_dist_samples<<<(c.s_r + 255) / 256, 256, 0, c.st>>>(c.keys, c.n_local, c.s_r, gbase, c.samples);
+    CUDA_OK(cudaGetLastError());
+    return GBS_SUCCESS;
+}
+
+// E4 sort the gathered p*s_r samples (identical on every rank), E5-E6 cut points
+gbs_status_t phase_cuts(const RankCtx& c)
+{
+    gbs_status_t r = gbs::sort_u64_inplace(c.gathered, (size_t)c.p * c.s_r, c.ws + c.L.u64ws, c.L.u64ws_bytes, c.st);
+    if (r) return r;
+    const uint64_t gbase = (uint64_t)c.rank * c.n_local;
+    k_dist_cuts<<<(c.p + 127) / 128, 128, 0, c.st>>>(c.keys, c.n_local, gbase, c.gathered, c.s_r, c.p, c.cuts);
+    CUDA_OK(cudaGetLastError());
+    return GBS_SUCCESS;
+}
+
+// E9: the p received runs (one per source rank, each sorted) -> one sorted run
+gbs_status_t phase_merge(const RankCtx& c, const uint64_t* recv_off, uint64_t total)
+{
+    std::vector<uint64_t> roff(c.p + 1);
+    for (int k = 0; k < c.p; ++k) roff[k] = recv_off[k];
+    roff[c.p] = total;
+    return gbs_merge_runs(c.out, roff.data(), c.p, c.ws, c.L.samples, c.st);
+}
+
+}  // namespace
+
+extern "C" {
+
 gbs_status_t gbs_sort_keys_dist(gbs_comm_t comm, uint32_t* d_keys, size_t n_local, uint32_t* d_out,
                                 size_t out_capacity, size_t* n_out, void* d_ws, size_t ws_bytes, gbs_stream_t stream)
 {
@@ -223,28 +296,16 @@ gbs_status_t gbs_sort_keys_dist(gbs_comm_t comm, uint32_t* d_keys, size_t n_loca
     if (ws_bytes < need) return gbs::fail_msg(GBS_ERROR_WORKSPACE_TOO_SMALL, "dist workspace too small");
     if (n_local == 0) { *n_out = 0; return GBS_SUCCESS; }
     cudaStream_t st = (cudaStream_t)stream;
-    DistLayout L;
-    dist_layout(n_local, p, &L);
-    char* w = reinterpret_cast<char*>(d_ws);
-    const size_t sort_ws = L.samples;
-    const uint32_t s_r = s_r_of(n_local);
-    const uint64_t gbase = (uint64_t)rank * n_local;
-    auto* samples = reinterpret_cast<unsigned long long*>(w + L.samples);
-    auto* gathered = reinterpret_cast<unsigned long long*>(w + L.gathered);
-    auto* cuts = reinterpret_cast<unsigned long long*>(w + L.cuts);
-    auto* all_cuts = reinterpret_cast<unsigned long long*>(w + L.all_cuts);
-
-    r = gbs_sort_keys(d_keys, n_local, w, sort_ws, stream);                            // E1
+    RankCtx c;
+    r = rank_ctx(c, d_keys, d_out, d_ws, n_local, p, rank, st);
     if (r) return r;
-    k_dist_samples<<<(s_r + 255) / 256, 256, 0, st>>>(d_keys, n_local, s_r, gbase, samples);  // E2
-    CUDA_OK(cudaGetLastError());
-    NCCL_OK(ncclAllGather(samples, gathered, s_r, ncclUint64, comm->nc, st));            // E3
-    r = gbs::sort_u64_inplace(gathered, (size_t)p * s_r, w + L.u64ws, L.u64ws_bytes, st);  // E4
+    r = phase_local(c);                                                                   // E1-E2
     if (r) return r;
-    k_dist_cuts<<<(p + 127) / 128, 128, 0, st>>>(d_keys, n_local, gbase, gathered, s_r, p, cuts);  // E5-E6
-    CUDA_OK(cudaGetLastError());
-    NCCL_OK(ncclAllGather(cuts, all_cuts, p, ncclUint64, comm->nc, st));                 // E7
-    CUDA_OK(cudaMemcpyAsync(comm->h_cuts, all_cuts, (size_t)p * p * 8, cudaMemcpyDeviceToHost, st));
+    NCCL_OK(ncclAllGather(c.samples, c.gathered, c.s_r, ncclUint64, comm->nc, st));      // E3
+    r = phase_cuts(c);                                                                    // E4-E6
+    if (r) return r;
+    NCCL_OK(ncclAllGather(c.cuts, c.all_cuts, p, ncclUint64, comm->nc, st));             // E7
+    CUDA_OK(cudaMemcpyAsync(comm->h_cuts, c.all_cuts, (size_t)p * p * 8, cudaMemcpyDeviceToHost, st));
     CUDA_OK(cudaStreamSynchronize(st));
     std::vector<uint64_t> so(p), sc(p), ro(p), rc(p);
     uint64_t total = 0;
@@ -261,14 +322,63 @@ gbs_status_t gbs_sort_keys_dist(gbs_comm_t comm, uint32_t* d_keys, size_t n_loca
     NCCL_OK(ncclGroupEnd());
     if (sc[rank])
         CUDA_OK(cudaMemcpyAsync(d_out + ro[rank], d_keys + so[rank], sc[rank] * 4, cudaMemcpyDeviceToDevice, st));
-    {   // E9: the p received runs (one per source rank, each sorted) -> one sorted run
-        std::vector<uint64_t> roff(p + 1);
-        for (int k = 0; k < p; ++k) roff[k] = ro[k];
-        roff[p] = total;
-        r = gbs_merge_runs(d_out, roff.data(), p, w, sort_ws, stream);
-    }
+    r = phase_merge(c, ro.data(), total);                                                // E9
     if (r) return r;
     *n_out = total;
+    return GBS_SUCCESS;
+}
+
+gbs_status_t gbs_sort_keys_dist_emulated(int p, uint32_t* d_keys, size_t n_local, uint32_t* d_out,
+                                         size_t out_capacity, size_t* n_out, void* d_ws, size_t ws_bytes,
+                                         gbs_stream_t stream)
+{
+    if (p < 1 || !n_out || (n_local && (!d_keys || !d_out)))
+        return gbs::fail_msg(GBS_ERROR_INVALID_VALUE, "gbs_sort_keys_dist_emulated: bad arguments");
+    size_t need = 0, cap = 0;
+    gbs_status_t r = gbs_sort_keys_dist_workspace_size(n_local, p, &need, &cap);
+    if (r) return r;
+    if (out_capacity < cap) return gbs::fail_msg(GBS_ERROR_INVALID_VALUE, "out_capacity below the receive bound");
+    if (ws_bytes < need) return gbs::fail_msg(GBS_ERROR_WORKSPACE_TOO_SMALL, "dist workspace too small");
+    if (n_local == 0) {
+        for (int k = 0; k < p; ++k) n_out[k] = 0;
+        return GBS_SUCCESS;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    std::vector<RankCtx> c(p);
+    for (int k = 0; k < p; ++k) {
+        r = rank_ctx(c[k], d_keys + (size_t)k * n_local, d_out + (size_t)k * out_capacity,
+                     reinterpret_cast<char*>(d_ws) + (size_t)k * ws_bytes, n_local, p, k, st);
+        if (r) return r;
+    }
+    for (int k = 0; k < p; ++k)                                                           // E1-E2
+        if ((r = phase_local(c[k]))) return r;
+    for (int k = 0; k < p; ++k)                                                           // E3 (allgather)
+        for (int q = 0; q < p; ++q)
+            CUDA_OK(cudaMemcpyAsync(c[k].gathered + (size_t)q * c[q].s_r, c[q].samples, (size_t)c[q].s_r * 8,
+                                    cudaMemcpyDeviceToDevice, st));
+    for (int k = 0; k < p; ++k)                                                           // E4-E6
+        if ((r = phase_cuts(c[k]))) return r;
+    std::vector<unsigned long long> all((size_t)p * p);                                   // E7 (allgather)
+    for (int q = 0; q < p; ++q)
+        CUDA_OK(cudaMemcpyAsync(all.data() + (size_t)q * p, c[q].cuts, (size_t)p * 8, cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaStreamSynchronize(st));
+    std::vector<std::vector<uint64_t>> so(p, std::vector<uint64_t>(p)), sc = so, ro = so, rc = so;
+    std::vector<uint64_t> total(p);
+    for (int k = 0; k < p; ++k) {
+        r = gbs_exchange_plan(reinterpret_cast<const uint64_t*>(all.data()), p, k, so[k].data(), sc[k].data(),
+                              ro[k].data(), rc[k].data(), &total[k]);
+        if (r) return r;
+        if (total[k] > out_capacity) return gbs::fail_msg(GBS_ERROR_CUDA, "receive count exceeds the proven bound");
+    }
+    for (int src = 0; src < p; ++src)                                                     // E8 (all-to-all)
+        for (int dst = 0; dst < p; ++dst)
+            if (sc[src][dst])
+                CUDA_OK(cudaMemcpyAsync(c[dst].out + ro[dst][src], c[src].keys + so[src][dst], sc[src][dst] * 4,
+                                        cudaMemcpyDeviceToDevice, st));
+    for (int k = 0; k < p; ++k) {                                                         // E9
+        if ((r = phase_merge(c[k], ro[k].data(), total[k]))) return r;
+        n_out[k] = total[k];
+    }
     return GBS_SUCCESS;
 }
 

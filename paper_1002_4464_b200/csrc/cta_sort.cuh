@@ -89,6 +89,13 @@ __device__ __forceinline__ void reg_sort(T (&x)[M])
     if constexpr (N > 1) apply_net<T, N, M>(x, std::make_index_sequence<BatcherNet<N>::C>{});
 }
 
+#ifndef GBS_SHFL_LEVELS
+#define GBS_SHFL_LEVELS 3   // first merge levels on warp shuffles, 4-byte items (0 = all through smem)
+#endif
+#ifndef GBS_SHFL_LEVELS_WIDE
+#define GBS_SHFL_LEVELS_WIDE 0   // the same for 8-byte items (u64 composites, pairs)
+#endif
+
 #ifndef GBS_PAD_SHIFT
 #define GBS_PAD_SHIFT 0   // 0 = one pad slot per ITEMS
 #endif
@@ -107,6 +114,9 @@ struct CtaSort {
     // independent merge chains per thread (ILP); overridable by the instantiation
     static constexpr int CHAINS = CHAINS_ > 0 ? CHAINS_ : ((ITEMS * sizeof(T) <= 256) ? 2 : 1);
     static constexpr T TMAX = ~T(0);
+    // merge levels done with warp shuffles (power-of-two ITEMS only)
+    static constexpr int SHFL_LEVELS =
+        ((ITEMS & (ITEMS - 1)) == 0 && ITEMS >= 2) ? (sizeof(T) == 4 ? GBS_SHFL_LEVELS : GBS_SHFL_LEVELS_WIDE) : 0;
 
     static __device__ __forceinline__ int phys(int p) { return p + (p >> PAD); }
     static __device__ __forceinline__ int phys_fma(int p) { return p + (p >> PAD); }
@@ -198,6 +208,47 @@ struct CtaSort {
                 a[c] = t ? v : a[c];
                 b[c] = t ? b[c] : v;
             }
+        }
+    }
+
+    // The first SHFL_LEVELS merge levels (runs of ITEMS -> ITEMS << SHFL_LEVELS, i.e.
+    // blocks of 2, 4, ... lanes) in registers with warp shuffles instead of shared
+    // memory: a bitonic merge of two ascending runs whose first half-cleaner pairs each
+    // item of the lower block with the mirror item of the upper one (folding in the
+    // reversal of the upper run), after which both halves are bitonic and the remaining
+    // half-cleaners (across lanes, then inside each lane) are all ascending.  On return
+    // lane l of each block holds positions [l ITEMS, (l+1) ITEMS) of the block's sorted
+    // run.  No shared-memory traffic and no merge-path search for these levels.
+    template <int M>
+    static __device__ __forceinline__ void warp_bitonic(T (&x)[M])
+    {
+        const int lane = threadIdx.x & 31;
+#pragma unroll
+        for (int j = 0; j < SHFL_LEVELS; ++j) {
+            const bool lower = !(lane & (1 << j));
+            const int mirror = (2 << j) - 1;
+#pragma unroll
+            for (int k = 0; k < ITEMS; ++k) {
+                const T a = lower ? x[k] : x[ITEMS - 1 - k];
+                const T r = __shfl_xor_sync(0xffffffffu, a, mirror);
+                const T v = lower ? (r < a ? r : a) : (r < a ? a : r);
+                if (lower) x[k] = v;
+                else x[ITEMS - 1 - k] = v;
+            }
+#pragma unroll
+            for (int q = j - 1; q >= 0; --q) {
+                const bool lo = !(lane & (1 << q));
+#pragma unroll
+                for (int k = 0; k < ITEMS; ++k) {
+                    const T r = __shfl_xor_sync(0xffffffffu, x[k], 1 << q);
+                    x[k] = lo ? (r < x[k] ? r : x[k]) : (r < x[k] ? x[k] : r);
+                }
+            }
+#pragma unroll
+            for (int d = ITEMS / 2; d >= 1; d /= 2)
+#pragma unroll
+                for (int k = 0; k < ITEMS; ++k)
+                    if ((k & d) == 0) cas(x[k], x[k + d]);
         }
     }
 
@@ -299,10 +350,13 @@ struct CtaSort {
     {
         const int t = threadIdx.x;
         const int wspan0 = (t >> 5) * WARP_SPAN;
-        if (wspan0 < valid) reg_sort<T, ITEMS, M>(x);
+        if (wspan0 < valid) {
+            reg_sort<T, ITEMS, M>(x);
+            if constexpr (SHFL_LEVELS > 0) warp_bitonic(x);
+        }
         const int start = t * ITEMS;
 #pragma unroll 1
-        for (int w = ITEMS; w < TILE; w *= 2) {
+        for (int w = ITEMS << SHFL_LEVELS; w < TILE; w *= 2) {
             const bool intra = 2 * w <= WARP_SPAN;
 #pragma unroll
             for (int k = 0; k < ITEMS; ++k) sm[phys(start + k)] = x[k];

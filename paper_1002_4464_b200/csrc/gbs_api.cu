@@ -256,6 +256,7 @@ static int build_node(Plan& P, int kind, uint32_t B, uint64_t N, uint32_t pad_ba
     nd.o_a = P.alloc(ms * 4);
     nd.o_l = P.alloc(ms * 4);
     nd.o_state = P.alloc((uint64_t)B * ((s + 31) / 32) * 8);
+    nd.o_pex = P.alloc(ms * 4);   // run starts P_i,j-1 (Step 6 -> grouped Step 8 / fused Step 8+9)
     if (own_reloc) {
         nd.o_reloc = P.alloc((uint64_t)B * N * key_bytes(kind));
         if (kind == KIND_PAIRS) nd.o_reloc_v = P.alloc((uint64_t)B * N * 4);
@@ -282,7 +283,6 @@ static int build_node(Plan& P, int kind, uint32_t B, uint64_t N, uint32_t pad_ba
         if (GBS_FUSE_89 && kind == KIND_KEYS && P.nodes[idx].m <= gather_max_m(kind) &&
             P.nodes[idx].d >= GBS_FUSE_MIN_D) {
             P.nodes[idx].fuse89 = true;
-            P.nodes[idx].o_pex = P.alloc(ms * 4);
         } else {
             P.launches += 1;  // relocate
         }
@@ -459,9 +459,31 @@ static void launch_index(const LevelDev& lv, cudaStream_t st)
     launch_k(k_sample_index<KIND, IDX_BLOCK>, lv.B * lv.m, IDX_BLOCK, sm, st, lv);
 }
 
+// Step 8 grouped by destination: sublists per group, per item kind (0 = one CTA per
+// sublist, k_relocate).  Measured: keys 8 (C2 Step 8 0.105 -> 0.085 ms, C3 0.258 ->
+// 0.159); pairs and the u64 sample levels measured slower grouped (C4; m = 128 at C2).
+#ifndef GBS_RELOC_GROUP_KEYS
+#define GBS_RELOC_GROUP_KEYS 8
+#endif
+#ifndef GBS_RELOC_GROUP_PAIRS
+#define GBS_RELOC_GROUP_PAIRS 0
+#endif
+#ifndef GBS_RELOC_GROUP_U64
+#define GBS_RELOC_GROUP_U64 0
+#endif
 template <int KIND>
 static void launch_relocate(const LevelDev& lv, cudaStream_t st)
 {
+    constexpr int GROUP = KIND == KIND_KEYS ? GBS_RELOC_GROUP_KEYS
+                                            : (KIND == KIND_PAIRS ? GBS_RELOC_GROUP_PAIRS : GBS_RELOC_GROUP_U64);
+    if constexpr (GROUP > 0) {
+        if (lv.pex) {     // run starts from Step 6
+            constexpr int G = GROUP, BLOCK = 256, JB = 64;
+            const unsigned grid = lv.B * ((lv.m + G - 1) / G) * ((lv.s + JB - 1) / JB);
+            launch_k(k_relocate_grouped<KIND, BLOCK, G, JB>, grid, BLOCK, 0, st, lv);
+            return;
+        }
+    }
     constexpr int MAXPER = (int)(tile_of_c(KIND) / IDX_BLOCK);
     const size_t per = std::max<size_t>(1, lv.L / IDX_BLOCK);
     const size_t sm = (size_t)2 * lv.s * 4 + (lv.L + 2 * (lv.L / per) + 4) * 2;
@@ -640,8 +662,8 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
     const bool fuse = nd.fuse89 && stop == 0 && !hp;
     lv.srt = lv.in;
     lv.srt_v = lv.in_v;
+    lv.pex = reinterpret_cast<uint32_t*>(ws + nd.o_pex);
     if (fuse) {
-        lv.pex = reinterpret_cast<uint32_t*>(ws + nd.o_pex);
         if (lv.in == lv.out) {
             lv.srt = lv.reloc;
             lv.srt_v = lv.reloc_v;

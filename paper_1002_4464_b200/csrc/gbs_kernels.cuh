@@ -1085,6 +1085,77 @@ __device__ __forceinline__ void segment_of(const LevelDev& lv, uint32_t idx, uin
     }
 }
 
+// Step 8, grouped by destination: a CTA per (group of G consecutive sublists, range of
+// JB buckets); a warp per bucket j copies the G runs (i, j) of its group, which are
+// adjacent in R (l_{i+1,j} = l_ij + a_ij, R5), as ONE contiguous destination chunk of
+// ~G d items.  Relocating sublist by sublist writes runs of ~d items at arbitrary
+// alignment whose partial 32-byte sectors each cost HBM a read-modify-write (measured:
+// DRAM reads 1.5x the algorithmic bytes at d = 16).  The run starts P_i,j-1 come from
+// Step 6 (lv.pex), so no row scan is needed and the grid is fine-grained.  Same R as
+// k_relocate, bit for bit.
+template <int KIND, int BLOCK, int G, int JB>
+__global__ void __launch_bounds__(BLOCK) k_relocate_grouped(LevelDev lv)
+{
+    pdl_entry();
+    using KT = typename std::conditional<KIND == KIND_U64, unsigned long long, uint32_t>::type;
+    __shared__ uint32_t sa[G][JB], sp[G][JB], sl[JB];
+    const uint32_t S = lv.s;
+    const uint32_t ng = (lv.m + G - 1) / G, nj = (S + JB - 1) / JB;
+    const uint32_t jb = blockIdx.x % nj, rest = blockIdx.x / nj;
+    const uint32_t b = rest / ng, i0 = (rest % ng) * G;
+    const uint32_t j0 = jb * JB, jn = min((uint32_t)JB, S - j0);
+    const int gn = (int)min((uint32_t)G, lv.m - i0);
+    const uint64_t row0 = ((uint64_t)b * lv.m + i0) * S + j0;
+    for (uint32_t t = threadIdx.x; t < (uint32_t)G * JB; t += BLOCK) {
+        const uint32_t r = t / JB, j = t % JB;
+        const bool ok = (int)r < gn && j < jn;
+        sa[r][j] = ok ? lv.a[row0 + (uint64_t)r * S + j] : 0u;
+        sp[r][j] = ok ? lv.pex[row0 + (uint64_t)r * S + j] : 0u;
+    }
+    for (uint32_t j = threadIdx.x; j < jn; j += BLOCK) sl[j] = lv.l[row0 + j];
+    __syncthreads();
+    const uint64_t off = lv.pr.offset(b);
+    const KT* src = reinterpret_cast<const KT*>(lv.srt) + off;
+    KT* dst = reinterpret_cast<KT*>(lv.reloc) + off;
+    const int lane = threadIdx.x & 31;
+    for (uint32_t j = threadIdx.x >> 5; j < jn; j += BLOCK / 32) {
+        uint32_t pre[G + 1], st[G];
+        pre[0] = 0;
+#pragma unroll
+        for (int r = 0; r < G; ++r) {
+            st[r] = (uint32_t)(i0 + r) * lv.L + sp[r][j];                // item index in the problem
+            pre[r + 1] = pre[r] + sa[r][j];
+        }
+        const uint32_t total = pre[G], d0 = sl[j];
+        for (uint32_t e0 = 0; e0 < total; e0 += 128) {                  // 4 loads in flight per lane
+            KT y[4];
+            uint32_t q[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t e = e0 + u * 32 + lane;
+                uint32_t base = st[0];
+#pragma unroll
+                for (int k = 1; k < G; ++k)
+                    if (e >= pre[k]) base = st[k] - pre[k];
+                q[u] = base + e;
+                if (e < total) y[u] = src[q[u]];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t e = e0 + u * 32 + lane;
+                if (e < total) dst[d0 + e] = y[u];
+            }
+            if (KIND == KIND_PAIRS) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t e = e0 + u * 32 + lane;
+                    if (e < total) lv.reloc_v[off + d0 + e] = lv.srt_v[off + q[u]];
+                }
+            }
+        }
+    }
+}
+
 // Step 9 size tiers: bucket idx goes to list t (0: 0 < v <= cut0, 1: cut0 < v <= cut1,
 // 2: v > cut1); empty buckets are dropped.  Each 256-bucket block appends its buckets in
 // index order (ballot compaction; one atomic per tier and block), so neighbouring CTAs

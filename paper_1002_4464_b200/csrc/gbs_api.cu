@@ -186,6 +186,7 @@ struct Plan {
 };
 
 static bool pow2(uint64_t x) { return x && !(x & (x - 1)); }
+static int reloc_launches(int kind);   // Step 8: 1, or 2 when both relocation forms are launched
 
 // Returns node index, or -1 with g_err set.
 static int build_node(Plan& P, int kind, uint32_t B, uint64_t N, uint32_t pad_base, const gbs_config_t* cfg,
@@ -255,7 +256,7 @@ static int build_node(Plan& P, int kind, uint32_t B, uint64_t N, uint32_t pad_ba
     nd.o_splitters = P.alloc((uint64_t)B * s * 8);
     nd.o_a = P.alloc(ms * 4);
     nd.o_l = P.alloc(ms * 4);
-    nd.o_state = P.alloc((uint64_t)B * ((s + 31) / 32) * 8);
+    nd.o_state = P.alloc((uint64_t)B * ((s + 31) / 32) * 8 + 8);   // + the longest-run word (Step 7)
     nd.o_pex = P.alloc(ms * 4);   // run starts P_i,j-1 (Step 6 -> grouped Step 8 / fused Step 8+9)
     if (own_reloc) {
         nd.o_reloc = P.alloc((uint64_t)B * N * key_bytes(kind));
@@ -284,12 +285,12 @@ static int build_node(Plan& P, int kind, uint32_t B, uint64_t N, uint32_t pad_ba
             P.nodes[idx].d >= GBS_FUSE_MIN_D) {
             P.nodes[idx].fuse89 = true;
         } else {
-            P.launches += 1;  // relocate
+            P.launches += reloc_launches(kind);
         }
     } else {
         P.nodes[idx].o_child_off = P.alloc((uint64_t)B * s * 8);
         P.nodes[idx].o_child_len = P.alloc((uint64_t)B * s * 4);
-        P.launches += 2;  // relocate + child descriptors
+        P.launches += reloc_launches(kind) + 1;  // relocate + child descriptors
         const uint64_t nb = (uint64_t)B * s;
         if (nb >= (1ull << 31)) { snprintf(g_err, sizeof g_err, "too many nested problems"); return -1; }
         const int c9 = build_node(P, kind, (uint32_t)nb, nd.hi, child_pad, nullptr, false);
@@ -471,17 +472,25 @@ static void launch_index(const LevelDev& lv, cudaStream_t st)
 #ifndef GBS_RELOC_GROUP_U64
 #define GBS_RELOC_GROUP_U64 0
 #endif
+static int reloc_launches(int kind)
+{
+    const int g = kind == KIND_KEYS ? GBS_RELOC_GROUP_KEYS : (kind == KIND_PAIRS ? GBS_RELOC_GROUP_PAIRS : GBS_RELOC_GROUP_U64);
+    return g > 0 ? 2 : 1;
+}
 template <int KIND>
 static void launch_relocate(const LevelDev& lv, cudaStream_t st)
 {
     constexpr int GROUP = KIND == KIND_KEYS ? GBS_RELOC_GROUP_KEYS
                                             : (KIND == KIND_PAIRS ? GBS_RELOC_GROUP_PAIRS : GBS_RELOC_GROUP_U64);
     if constexpr (GROUP > 0) {
-        if (lv.pex) {     // run starts from Step 6
+        if (lv.pex && lv.maxrun) {
+            // Both forms are launched; each reads Step 7's longest run and one exits at
+            // once: grouped by destination when runs are short (spread inputs), one CTA
+            // per sublist when some run is long (sorted / clustered inputs), where the
+            // grouped form would leave whole buckets to single warps (R21).
             constexpr int G = GROUP, BLOCK = 256, JB = 64;
             const unsigned grid = lv.B * ((lv.m + G - 1) / G) * ((lv.s + JB - 1) / JB);
             launch_k(k_relocate_grouped<KIND, BLOCK, G, JB>, grid, BLOCK, 0, st, lv);
-            return;
         }
     }
     constexpr int MAXPER = (int)(tile_of_c(KIND) / IDX_BLOCK);
@@ -489,7 +498,9 @@ static void launch_relocate(const LevelDev& lv, cudaStream_t st)
     const size_t sm = (size_t)2 * lv.s * 4 + (lv.L + 2 * (lv.L / per) + 4) * 2;
     static std::once_flag f;
     std::call_once(f, [&] { set_smem(k_relocate<KIND, IDX_BLOCK, MAXPER>, 220 * 1024); });
-    launch_k(k_relocate<KIND, IDX_BLOCK, MAXPER>, lv.B * lv.m, IDX_BLOCK, sm, st, lv);
+    LevelDev lr = lv;   // the per-sublist form defers to the grouped one only if that was launched
+    if (!(GROUP > 0 && lv.pex)) lr.maxrun = nullptr;
+    launch_k(k_relocate<KIND, IDX_BLOCK, MAXPER>, lv.B * lv.m, IDX_BLOCK, sm, st, lr);
 }
 
 static uint32_t num_sms()
@@ -756,7 +767,8 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
 
     // Step 7: column-major exclusive scan -> l
     const unsigned nblk = (nd.s + 31) / 32;
-    GBS_CUDA(cudaMemsetAsync(lv.state, 0, (size_t)nd.B * nblk * 8, st));
+    lv.maxrun = reinterpret_cast<uint32_t*>(lv.state + (size_t)nd.B * nblk);   // one word past the look-back words
+    GBS_CUDA(cudaMemsetAsync(lv.state, 0, (size_t)nd.B * nblk * 8 + 8, st));
     launch_k(k_scan, nd.B * nblk, SCAN_BLOCK, 0, st, lv);
     GBS_LAUNCHED();
     if (stop == 7) return GBS_SUCCESS;

@@ -31,6 +31,10 @@ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < 
 // predecessor's completion (and memory) before touching global memory.  The successor
 // thus fills the SMs the predecessor's last wave frees instead of waiting for the
 // launch after the grid drains.  No-ops for a normal launch.
+#ifndef GBS_GROUP_MAX_RUN
+#define GBS_GROUP_MAX_RUN 256   // grouped Step 8 only when every run a_ij is at most this long
+#endif
+
 __device__ __forceinline__ void pdl_entry()
 {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -82,6 +86,9 @@ struct LevelDev {
     // host-pipelined calls (gbs_sort_keys_host): k_local_sort sorts tiles [tile_lo,
     // tile_hi) and k_segment_sort the segments [seg_lo, seg_hi) of the level (0, 0 = all)
     uint32_t tile_lo, tile_hi, seg_lo, seg_hi;
+    // Step 7 records the longest run max a_ij here (zeroed with the look-back words);
+    // Step 8 picks the grouped relocation only when runs are short (R21)
+    uint32_t* maxrun;
 };
 
 // L2 prefetch of a byte range (cp.async.bulk.prefetch: a TMA bulk operation, no
@@ -839,7 +846,7 @@ __global__ void __launch_bounds__(SCAN_BLOCK) k_scan(LevelDev lv)
     const uint32_t* A = lv.a + (uint64_t)b * lv.m * lv.s;
     uint32_t* Lo = lv.l + (uint64_t)b * lv.m * lv.s;
 
-    uint32_t sum = 0;
+    uint32_t sum = 0, mx = 0;
     if (col_ok) {
         uint64_t r = r0;
         for (; r + 8 <= r1; r += 8) {           // 8 independent loads in flight
@@ -847,9 +854,14 @@ __global__ void __launch_bounds__(SCAN_BLOCK) k_scan(LevelDev lv)
 #pragma unroll
             for (int u = 0; u < 8; ++u) x[u] = A[(r + u) * lv.s + c];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) sum += x[u];
+            for (int u = 0; u < 8; ++u) { sum += x[u]; mx = max(mx, x[u]); }
         }
-        for (; r < r1; ++r) sum += A[r * lv.s + c];
+        for (; r < r1; ++r) { const uint32_t x = A[r * lv.s + c]; sum += x; mx = max(mx, x); }
+    }
+    if (lv.maxrun) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (lane == 0 && mx) atomicMax(lv.maxrun, mx);
     }
     wsum[w][lane] = sum;
     __syncthreads();
@@ -959,6 +971,7 @@ template <int KIND, int BLOCK, int MAXPER>
 __global__ void __launch_bounds__(BLOCK, 2) k_relocate(LevelDev lv)
 {
     pdl_entry();
+    if (lv.maxrun && *lv.maxrun <= GBS_GROUP_MAX_RUN) return;   // short runs: k_relocate_grouped did it
     using KT = typename std::conditional<KIND == KIND_U64, unsigned long long, uint32_t>::type;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     uint32_t* starts = reinterpret_cast<uint32_t*>(smem_raw);
@@ -1097,6 +1110,7 @@ template <int KIND, int BLOCK, int G, int JB>
 __global__ void __launch_bounds__(BLOCK) k_relocate_grouped(LevelDev lv)
 {
     pdl_entry();
+    if (lv.maxrun && *lv.maxrun > GBS_GROUP_MAX_RUN) return;    // long runs: k_relocate does it
     using KT = typename std::conditional<KIND == KIND_U64, unsigned long long, uint32_t>::type;
     __shared__ uint32_t sa[G][JB], sp[G][JB], sl[JB];
     const uint32_t S = lv.s;

@@ -128,6 +128,9 @@ struct Node {
     size_t o_tiers = 0;   // Step 9 size-tier lists (3 x B*s) + counters (4)
     size_t o_pex = 0;     // fused Step 8+9: run starts P_i,j-1 (B*m*s)
     bool fuse89 = false;  // Step 9 gathers straight from the sorted sublists (no Step 8 pass)
+    bool s4_tree = false; // Step 4 as a merge tree (R22) instead of a u64 level
+    int s4_levels = 0;    // its global merge levels (between the tile merge and the selection)
+    size_t o_s4tmp = 0;   // its ping-pong buffer (m*s u64)
 };
 
 // big / small CTA configurations per kind
@@ -184,6 +187,17 @@ struct Plan {
         return o;
     }
 };
+
+#ifndef GBS_S4_TREE
+#define GBS_S4_TREE 1     // Step 4 of one problem with <= GBS_S4_TREE_MAX samples as a merge tree (R22)
+#endif
+#ifndef GBS_S4_TREE_MAX
+#define GBS_S4_TREE_MAX (1u << 23)   // 64 MB of composites: L2-resident (126 MB)
+#endif
+#ifndef GBS_S4_TILE_BLOCK
+#define GBS_S4_TILE_BLOCK 1024        // tile merge CTA: x 16 u64 per thread
+#endif
+constexpr uint32_t S4_TILE = GBS_S4_TILE_BLOCK * 16;
 
 static bool pow2(uint64_t x) { return x && !(x & (x - 1)); }
 static int reloc_launches(int kind);   // Step 8: 1, or 2 when both relocation forms are launched
@@ -266,9 +280,19 @@ static int build_node(Plan& P, int kind, uint32_t B, uint64_t N, uint32_t pad_ba
     const int idx = (int)P.nodes.size();
     P.nodes.push_back(nd);
     const uint32_t child_pad = kind == KIND_U64 ? pad_base + (uint32_t)(nd.Np - N) : (uint32_t)nd.Np;
-    const int c4 = build_node(P, KIND_U64, B, (uint64_t)nd.m * s, child_pad, nullptr, true);
-    if (c4 < 0) return -1;
-    P.nodes[idx].step4 = c4;
+    if (GBS_S4_TREE && B == 1 && ms > S4_TILE && ms <= GBS_S4_TREE_MAX) {
+        // Step 4 as a merge tree (R22): tile merge, global pair levels until two runs are
+        // left, then the selection of the s splitters
+        Node& me = P.nodes[idx];
+        me.s4_tree = true;
+        me.o_s4tmp = P.alloc(ms * 8);
+        for (uint64_t R = S4_TILE; 2 * R < ms; R *= 2) ++me.s4_levels;
+        P.launches += 2 + me.s4_levels;
+    } else {
+        const int c4 = build_node(P, KIND_U64, B, (uint64_t)nd.m * s, child_pad, nullptr, true);
+        if (c4 < 0) return -1;
+        P.nodes[idx].step4 = c4;
+    }
     if (nd.hi <= tile) {
         P.nodes[idx].bucket_small = nd.hi <= SMALL_TILE;
         // buckets that may exceed half a tile: size tiers (see exec_kind)
@@ -320,6 +344,7 @@ static gbs_status_t make_plan(size_t n, int kind, const gbs_config_t* cfg, Plan&
 
 // ----------------------------------------------------------------- launches
 static uint32_t num_sms();
+constexpr int S4_MERGE_BLOCK = 256, S4_MERGE_ITEMS = 16;
 #ifndef GBS_SPLIT_STEP9
 #define GBS_SPLIT_STEP9 1
 #endif
@@ -563,6 +588,40 @@ static gbs_status_t exec(const Plan& P, int ni, char* ws, const Bufs& bf, Probs 
     }
 }
 
+// Step 4 as a merge tree (R22): the m runs of s samples -> runs of TILE_U64 on chip, pair
+// levels to two runs, then the s splitters by selection (full: the last level merges
+// everything, for stage parity of the sorted samples).  The last level reads the tmp
+// buffer and writes the samples array, so the tile merge starts on whichever buffer makes
+// the G pair levels end in tmp.
+static gbs_status_t launch_s4_tree(const Node& nd, const LevelDev& lv, char* ws, cudaStream_t st, bool full)
+{
+    constexpr int KIND = KIND_U64;   // (GBS_LAUNCHED reports the node kind)
+    constexpr int TB = GBS_S4_TILE_BLOCK, TI = 16, TILE = TB * TI;
+    const uint32_t N = nd.m * nd.s;
+    u64* S = lv.samples;
+    u64* T = reinterpret_cast<u64*>(ws + nd.o_s4tmp);
+    u64* cur = (nd.s4_levels % 2 == 0) ? T : S;
+    u64* oth = cur == T ? S : T;
+    const size_t sm = sizeof(u64) * CtaSort<unsigned long long, TB, TI>::SMEM_ELEMS;
+    static std::once_flag f;
+    std::call_once(f, [&] { set_smem(k_s4_tile<TB, TI>, sm); });
+    launch_k(k_s4_tile<TB, TI>, (N + TILE - 1) / TILE, TB, sm, st, (const u64*)S, cur, N, nd.s);
+    GBS_LAUNCHED();
+    constexpr uint32_t TO = S4_MERGE_BLOCK * S4_MERGE_ITEMS;
+    const unsigned mgrid = (N + TO - 1) / TO;
+    uint32_t R = TILE;
+    for (int g = 0; g < nd.s4_levels; ++g, R *= 2) {
+        launch_k(k_s4_merge<S4_MERGE_BLOCK, S4_MERGE_ITEMS>, mgrid, S4_MERGE_BLOCK, 0, st, (const u64*)cur, oth, N, R);
+        GBS_LAUNCHED();
+        std::swap(cur, oth);
+    }
+    if (cur != T) return fail(GBS_ERROR_CUDA, "internal: merge tree parity");
+    if (full) launch_k(k_s4_merge<S4_MERGE_BLOCK, S4_MERGE_ITEMS>, mgrid, S4_MERGE_BLOCK, 0, st, (const u64*)T, S, N, R);
+    else launch_k(k_s4_select, (nd.s * 32 + 255) / 256, 256, 0, st, (const u64*)T, S, N, R, nd.m, nd.s);
+    GBS_LAUNCHED();
+    return GBS_SUCCESS;
+}
+
 // Step 9 over CTA buckets: one launch, or the size tiers (MODE_BUCKET reads the
 // relocated buckets, MODE_GATHER gathers them from the sorted sublists)
 template <int KIND, int MODE>
@@ -722,8 +781,12 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
     if (stop == 2 || stop == 3) return GBS_SUCCESS;
     pm.mark();
 
-    // Step 4: sort the B*m*s samples = a U64 level on B problems of m*s composites
-    {
+    // Step 4: sort the B*m*s samples = a U64 level on B problems of m*s composites, or
+    // (one problem, L2-resident samples) a merge tree of the m presorted runs of s
+    if (nd.s4_tree) {
+        gbs_status_t r = launch_s4_tree(nd, lv, ws, st, stop == 4 || stop == 5);
+        if (r) return r;
+    } else {
         const Node& c = P.nodes[nd.step4];
         Bufs b4{lv.samples, c.leaf ? (void*)lv.samples : (void*)(ws + c.o_reloc), lv.samples, nullptr, nullptr, nullptr};
         // each sublist's s samples are sorted and contiguous: runs of length s
@@ -751,7 +814,7 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
         unsigned* dflag = nullptr;
         GBS_CUDA(cudaMallocManaged(&dflag, 8 * sizeof(unsigned)));
         memset(dflag, 0, 8 * sizeof(unsigned));
-        launch_k(k_check_level, 1024, 256, 0, st, lv, dflag);
+        launch_k(k_check_level, 1024, 256, 0, st, lv, dflag, (int)(nd.s4_tree && !(stop == 4 || stop == 5)));
         GBS_CUDA(cudaStreamSynchronize(st));
         unsigned fl[8];
         memcpy(fl, dflag, sizeof fl);

@@ -559,6 +559,155 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BLOCK, 1) k_local_so
     }
 }
 
+// ------------------------------------------------------------ Step 4 as a merge tree
+// Step 4 sorts the m*s samples, and Step 5 reads s of them:
+// g_k = sorted[(k+1)m - 1] (R2).  The samples arrive as m sorted runs of s
+// (Step 3 takes them from sorted sublists), so sorting them is a merge of m runs.  For
+// one problem whose samples stay L2-resident (R22): k_s4_tile merges the runs inside
+// tiles of TILE_U64 on chip, k_s4_merge merges pairs of runs per launch (one CTA per
+// output tile, the merge-path split found by a warp), and once two runs are left
+// k_s4_select computes only the s order statistics Step 5 reads, each by one merge-path
+// split: the d-th output of merge(A, B) is max(A[i-1], B[d-1-i]), i = split(d).
+
+// Merge-path split of diagonal d in merge(A[0, na), B[0, nb)): the number of A items among
+// the first d outputs (ties: A first).  One warp, 32 evenly spaced probes per round:
+// P(i) = A[i] <= B[d-1-i] is true below the split and false from it on, so the ballot's
+// popcount c narrows the interval to the c-th gap (log_32 of the range rounds, each one
+// pair of L2 loads per lane).  All lanes return the split.
+__device__ __forceinline__ uint32_t warp_split(const u64* A, uint32_t na, const u64* B, uint32_t nb, uint32_t d)
+{
+    const uint32_t lane = threadIdx.x & 31;
+    uint32_t lo = d > nb ? d - nb : 0, hi = min(d, na);   // split in [lo, hi]
+    while (lo < hi) {
+        const uint32_t step = (hi - lo + 31) / 32;
+        const uint32_t p = lo + (lane + 1) * step - 1;
+        const bool t = p < hi && A[p] <= B[d - 1 - p];
+        const uint32_t c = __popc(__ballot_sync(0xffffffffu, t));
+        hi = min(hi, lo + (c + 1) * step - 1);   // P false at probe c (when it exists)
+        lo += c * step;                          // P true at probe c-1
+    }
+    return lo;
+}
+
+// Runs of R (a power of two, R >= ITEMS: merge levels only; R < ITEMS: full sort) merged
+// inside tiles of TILE: src -> dst (may alias: a CTA reads its whole tile first).
+template <int BLOCK, int ITEMS>
+__global__ void __launch_bounds__(BLOCK, 1) k_s4_tile(const u64* src, u64* dst, uint32_t N, uint32_t R)
+{
+    pdl_entry();
+    using CS = CtaSort<unsigned long long, BLOCK, ITEMS>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    unsigned long long* sm = reinterpret_cast<unsigned long long*>(smem_raw);
+    const uint64_t t0 = (uint64_t)blockIdx.x * CS::TILE;
+    const int v = (int)umin64(CS::TILE, N - t0);
+    unsigned long long x[ITEMS];
+    if (R >= (uint32_t)ITEMS) {
+        CS::sort_presorted(x, src + t0, sm, v, (int)R);
+    } else {
+        CS::load(x, src + t0, v);
+        CS::sort(x, sm, v);
+    }
+    for (int p = threadIdx.x; p < v; p += BLOCK) dst[t0 + p] = sm[CS::phys(p)];
+}
+
+// One merge level: pairs of runs of R (run r = [rR, min((r+1)R, N)); an unpaired last run
+// is copied through) -> runs of 2R.  CTA = TO consecutive outputs inside one pair; the
+// splits of its first and last diagonals by two warps, both input ranges staged in
+// shared memory, a merge-path merge of ITEMS outputs per thread, a padded transpose for
+// coalesced stores.  Ties take A first (stable; the composites are distinct anyway).
+#ifndef GBS_S4_MERGE_MINB
+#define GBS_S4_MERGE_MINB 4   // CTAs per SM (registers): the whole level in one wave
+#endif
+template <int BLOCK, int ITEMS>
+__global__ void __launch_bounds__(BLOCK, GBS_S4_MERGE_MINB) k_s4_merge(const u64* src, u64* dst, uint32_t N, uint32_t R)
+{
+    pdl_entry();
+    constexpr int TO = BLOCK * ITEMS;
+    __shared__ u64 sm[TO + TO / ITEMS + ITEMS];
+    __shared__ uint32_t s_split[2];
+    const uint64_t o0 = (uint64_t)blockIdx.x * TO;
+    if (o0 >= N) return;
+    const uint64_t base = o0 / (2ull * R) * (2ull * R);
+    const uint32_t na = (uint32_t)umin64(R, N - base);
+    const uint32_t nb = (uint32_t)(N - base > R ? umin64(R, N - base - R) : 0);
+    const u64* A = src + base;
+    const u64* Bp = A + na;
+    const uint32_t d0 = (uint32_t)(o0 - base), d1 = min(d0 + (uint32_t)TO, na + nb);
+    const int warp = threadIdx.x >> 5;
+    if (warp < 2) {
+        const uint32_t sp = warp_split(A, na, Bp, nb, warp ? d1 : d0);
+        if ((threadIdx.x & 31) == 0) s_split[warp] = sp;
+    }
+    __syncthreads();
+    const uint32_t a0 = s_split[0], a1 = s_split[1];
+    const int la = (int)(a1 - a0), lb = (int)((d1 - a1) - (d0 - a0)), tot = la + lb;
+    const u64* As = A + a0;
+    const u64* Bs = Bp + (d0 - a0);
+    u64 out[ITEMS];
+    // staging: all ITEMS loads of a thread in flight before the shared-memory stores
+#pragma unroll
+    for (int r = 0; r < ITEMS; ++r) {
+        const int i = threadIdx.x + r * BLOCK;
+        out[r] = i < la ? __ldg(As + i) : (i < tot ? __ldg(Bs + (i - la)) : 0ull);
+    }
+#pragma unroll
+    for (int r = 0; r < ITEMS; ++r) {
+        const int i = threadIdx.x + r * BLOCK;
+        if (i < tot) sm[i] = out[r];
+    }
+    __syncthreads();
+    const int dg = threadIdx.x * ITEMS;
+    if (dg < tot) {
+        int lo = max(0, dg - lb), hi = min(dg, la);
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (sm[mid] <= sm[la + dg - 1 - mid]) lo = mid + 1;
+            else hi = mid;
+        }
+        // one shared-memory load per output: the head of the run just consumed; an
+        // exhausted run reads as all-ones (never a composite: tags < 2^32 - 2^20)
+        int i = lo, j = dg - lo;
+        u64 a = i < la ? sm[i] : ~0ull, b = j < lb ? sm[la + j] : ~0ull;
+#pragma unroll
+        for (int r = 0; r < ITEMS; ++r) {
+            const bool t = a <= b;
+            out[r] = t ? a : b;
+            i += t ? 1 : 0;
+            j += t ? 0 : 1;
+            const bool ok = t ? i < la : j < lb;
+            const u64 v = sm[ok ? (t ? i : la + j) : 0];
+            a = t ? (ok ? v : ~0ull) : a;
+            b = t ? b : (ok ? v : ~0ull);
+        }
+    }
+    __syncthreads();
+    if (dg < tot) {
+#pragma unroll
+        for (int r = 0; r < ITEMS; ++r) {
+            const int o = dg + r;
+            sm[o + o / ITEMS] = out[r];
+        }
+    }
+    __syncthreads();
+    u64* C = dst + o0;
+    for (int o = threadIdx.x; o < tot; o += BLOCK) C[o] = sm[o + o / ITEMS];
+}
+
+// The last level, selection only: with runs A = src[0, R) and B = src[R, N) (N <= 2R),
+// samples[(k+1)m - 1] = the ((k+1)m)-th smallest of A u B, one warp per k < s.
+__global__ void k_s4_select(const u64* src, u64* samples, uint32_t N, uint32_t R, uint32_t m, uint32_t s)
+{
+    pdl_entry();
+    const uint32_t k = (uint32_t)(((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    if (k >= s) return;   // warp-uniform
+    const uint32_t d = (k + 1) * m;
+    const uint32_t na = min(R, N), nb = N - na;
+    const uint32_t i = warp_split(src, na, src + na, nb, d);
+    u64 g = i > 0 ? src[i - 1] : 0ull;
+    if (d > i) g = max(g, src[na + (d - i - 1)]);
+    if ((threadIdx.x & 31) == 0) samples[(uint64_t)d - 1] = g;
+}
+
 // ------------------------------------------------------------ Step 5
 // Global sampling: g_k = sorted_samples[(k+1)m - 1] (R2).
 __global__ void k_global_samples(LevelDev lv)
@@ -1317,13 +1466,19 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK <= 512 ? 2 : 1)) k_segment_sort(
 // Debug-only invariant checks (GBS_DEBUG_SYNC): *flag |= 1 if some problem's sorted
 // samples are out of order, |= 2 if some row of a does not sum to the sublist's
 // real item count (conservation).
-__global__ void k_check_level(LevelDev lv, unsigned* flag)
+// With a selection-only Step 4 (k_s4_select) only the splitter positions are checked.
+__global__ void k_check_level(LevelDev lv, unsigned* flag, int only_splitters)
 {
     pdl_entry();
     const uint64_t ms = (uint64_t)lv.m * lv.s;
     for (uint64_t q = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; q < (uint64_t)lv.B * ms;
          q += (uint64_t)gridDim.x * blockDim.x) {
-        if (q % ms != 0 && lv.samples[q] <= lv.samples[q - 1]) atomicOr(flag, 1u);
+        if (only_splitters) {
+            const uint64_t r = q % ms + 1;
+            if (r % lv.m == 0 && r > lv.m && lv.samples[q] <= lv.samples[q - lv.m]) atomicOr(flag, 1u);
+        } else if (q % ms != 0 && lv.samples[q] <= lv.samples[q - 1]) {
+            atomicOr(flag, 1u);
+        }
         if (q % lv.s == 0) {
             const uint64_t row = q / lv.s;
             const uint32_t b = (uint32_t)(row / lv.m), i = (uint32_t)(row % lv.m);

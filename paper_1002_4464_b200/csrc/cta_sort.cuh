@@ -96,6 +96,10 @@ __device__ __forceinline__ void reg_sort(T (&x)[M])
 #define GBS_SHFL_LEVELS_WIDE 0   // the same for 8-byte items (u64 composites, pairs)
 #endif
 
+#ifndef GBS_NARROW_SPLIT
+#define GBS_NARROW_SPLIT 1   // merge chains after the first search a window of H + 1 for their split
+#endif
+
 #ifndef GBS_PAD_SHIFT
 #define GBS_PAD_SHIFT 0   // 0 = one pad slot per ITEMS
 #endif
@@ -134,8 +138,12 @@ struct CtaSort {
     // B = [a0+w, a0+2w)): number of outputs taken from A (ties: A first -> stable).
     static __device__ __forceinline__ int split(const T* sm, int a0, int w, int diag)
     {
+        return split_in(sm, a0, w, diag, max(0, diag - w), min(diag, w));
+    }
+    // the same, knowing the split lies in [lo, hi]
+    static __device__ __forceinline__ int split_in(const T* sm, int a0, int w, int diag, int lo, int hi)
+    {
         const int b0 = a0 + w;
-        int lo = max(0, diag - w), hi = min(diag, w);
         while (lo < hi) {
             const int mid = (lo + hi) >> 1;
             if (sm[phys(a0 + mid)] <= sm[phys(b0 + diag - 1 - mid)]) lo = mid + 1;
@@ -163,10 +171,15 @@ struct CtaSort {
         const int aEnd = base + w, bEnd = base + 2 * w;
         int ai[CHAINS], cb[CHAINS];
         T a[CHAINS], b[CHAINS];
+        // chain c's split lies in [split(c-1), split(c-1) + H]: H more outputs take at most
+        // H more items of A, so only the first chain searches the whole diagonal
+        int sp = 0;
 #pragma unroll
         for (int c = 0; c < CHAINS; ++c) {
             const int diag = start - base + c * H;
-            ai[c] = base + split(sm, base, w, diag);
+            sp = c == 0 || !GBS_NARROW_SPLIT ? split(sm, base, w, diag)
+                                             : split_in(sm, base, w, diag, max(sp, diag - w), min(sp + H, min(diag, w)));
+            ai[c] = base + sp;
             cb[c] = 2 * base + w + diag;              // bi = cb - ai
             const int bi = cb[c] - ai[c];
             a[c] = ai[c] < aEnd ? sm[phys(ai[c])] : TMAX;

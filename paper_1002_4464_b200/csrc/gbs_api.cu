@@ -425,6 +425,18 @@ static void launch_seg_t(const LevelDev& lv, unsigned count, cudaStream_t st)
 }
 
 
+#ifndef GBS_RARE_PERSIST
+#define GBS_RARE_PERSIST 1   // Step 9's full-tile tier on persistent CTAs (k_segment_sort_rare)
+#endif
+template <int KIND, int BLOCK, int ITEMS>
+static void launch_rare_t(const LevelDev& lv, unsigned count, cudaStream_t st)
+{
+    const size_t sm = Seg<KIND, BLOCK, ITEMS>::smem_bytes();
+    static std::once_flag f;
+    std::call_once(f, [&] { set_smem(k_segment_sort_rare<KIND, BLOCK, ITEMS>, sm); });
+    launch_k(k_segment_sort_rare<KIND, BLOCK, ITEMS>, std::min<unsigned>(count, num_sms()), BLOCK, sm, st, lv);
+}
+
 // Step 2 on CTA pairs: persistent clusters of two (one CTA per SM)
 static void launch_local_pair(const LevelDev& lv, cudaStream_t st)
 {
@@ -664,8 +676,13 @@ static gbs_status_t launch_step9(const LevelDev& lv, const Node& nd, char* ws, c
             cudaStream_t s12 = ss ? ss : st;
             if (GBS_MID_STEP9) {
                 if (nd.hi > cut1) {
-                    if constexpr (KIND == KIND_KEYS) launch_seg_t<KIND, GBS_BIG_KEYS, MODE>(t2, count, s12);
-                    else launch_seg_t<KIND, GBS_BIG_WIDE, MODE>(t2, count, s12);
+                    if constexpr (MODE == MODE_BUCKET && GBS_RARE_PERSIST) {
+                        if constexpr (KIND == KIND_KEYS) launch_rare_t<KIND, GBS_BIG_KEYS>(t2, count, s12);
+                        else launch_rare_t<KIND, GBS_BIG_WIDE>(t2, count, s12);
+                    } else {
+                        if constexpr (KIND == KIND_KEYS) launch_seg_t<KIND, GBS_BIG_KEYS, MODE>(t2, count, s12);
+                        else launch_seg_t<KIND, GBS_BIG_WIDE, MODE>(t2, count, s12);
+                    }
                     GBS_LAUNCHED();
                 }
                 launch_seg_t<KIND, MID_BLOCK_OF(KIND), MID_ITEMS_OF(KIND), MODE>(t1, count, s12);

@@ -1463,6 +1463,26 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK <= 512 ? 2 : 1)) k_segment_sort(
     A::run(src, src_v, off, v, lv.out, lv.out_v, smem_raw);
 }
 
+// The full-tile size tier of Step 9 (buckets above 5/8 of a tile: rare, none for
+// uniform inputs) on persistent CTAs, one per SM, walking the tier's list: an empty
+// tier then costs one wave of CTAs that exit at once instead of one CTA per bucket slot
+// (whose 133 KB of shared memory each would block the concurrent small tier's CTAs).
+template <int KIND, int BLOCK, int ITEMS>
+__global__ void __launch_bounds__(BLOCK, 1) k_segment_sort_rare(LevelDev lv)
+{
+    pdl_entry();
+    using A = Adapt<KIND, BLOCK, ITEMS, GBS_ADAPT_DEPTH>;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const uint32_t len = *lv.tier_len;
+    for (uint32_t q = blockIdx.x; q < len; q += gridDim.x) {
+        if (q != blockIdx.x) __syncthreads();   // shared memory reused
+        uint64_t off;
+        int v;
+        segment_of<MODE_BUCKET>(lv, lv.tier_list[q], off, v);
+        A::run(lv.reloc, lv.reloc_v, off, v, lv.out, lv.out_v, smem_raw);
+    }
+}
+
 // Debug-only invariant checks (GBS_DEBUG_SYNC): *flag |= 1 if some problem's sorted
 // samples are out of order, |= 2 if some row of a does not sum to the sublist's
 // real item count (conservation).

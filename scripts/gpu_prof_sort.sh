@@ -1,2 +1,3 @@
 python -c "from paper_1002_4464_b200 import _build; _build.build()"
-timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k 'regex:k_(local_sort|segment_sort)<.int.0,' -c 2 -o gpurun_out/prof_sort2 python bench.py --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/ncu_sort.log 2>&1; echo ncu rc=$?
+B="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_local_sort|k_segment_sort|k_relocate_grouped|k_sample_index_tma|k_s4_" -c 12 -o gpurun_out/prof_sort $B > gpurun_out/ncu_sort.log 2>&1; echo ncu rc=$?

@@ -128,6 +128,22 @@ def traffic_from_profile(step_kernel: str):
         return None
 
 
+def limiter_from_profile(step_kernel: str):
+    """What bounds the dominant kernel, from the committed ncu --set full summary: issue
+    slots, ALU pipe, shared-memory wavefronts (percent of peak) and the top stall."""
+    path = os.path.join(ROOT, "profiles", "ncu_full_summary.json")
+    try:
+        with open(path) as f:
+            k = json.load(f)["kernels"][step_kernel]
+        return {"issue_active_pct": round(k["smsp__issue_active.avg.pct_of_peak_sustained_active"], 1),
+                "alu_pipe_pct": round(k["sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"], 1),
+                "smem_wavefronts_pct": round(
+                    k["l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"], 1),
+                "top_stall": k["top_stalls"][0][0], "source": "profiles/ncu_full_summary.json (ncu --set full)"}
+    except Exception:  # noqa: BLE001
+        return None
+
+
 def algorithmic_bytes(n: int, plan: dict, ib: int = 4):
     """Bytes each level-1 step must move; ib = 4 keys, 8 pairs."""
     L, s = plan["levels"][0]
@@ -145,7 +161,7 @@ def algorithmic_bytes(n: int, plan: dict, ib: int = 4):
     }
 
 
-STEP_NAMES = {2: "k_local_sort (Steps 2-3)", 4: "Step 4 (recursive sample sort)", 5: "k_global_samples (Step 5)",
+STEP_NAMES = {2: "k_local_sort (Steps 2-3)", 4: "Step 4 (sample sort: merge tree or u64 level)", 5: "k_global_samples (Step 5)",
               6: "k_sample_index (Step 6)", 7: "k_scan (Step 7)", 8: "k_relocate (Step 8)",
               9: "k_segment_sort (Step 9)"}
 
@@ -420,7 +436,8 @@ def main():
         roof = {"bound": "hbm", "kernel": STEP_NAMES[dom], "achieved": round(ach, 1), "peak": peak,
                 "unit": "GB/s", "frac": round(ach / peak, 4), "peak_source": peak_src,
                 "traffic": traffic_from_profile(STEP_NAMES[dom].split()[0]),
-                "alg_bytes_per_launch": ab[dom], "launch_ms": round(t_ms, 4)}
+                "alg_bytes_per_launch": ab[dom], "launch_ms": round(t_ms, 4),
+                "limiter": limiter_from_profile(STEP_NAMES[dom].split()[0])}
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:

@@ -1282,11 +1282,13 @@ __global__ void __launch_bounds__(BLOCK) k_relocate_grouped(LevelDev lv)
     KT* dst = reinterpret_cast<KT*>(lv.reloc) + off;
     const int lane = threadIdx.x & 31;
     for (uint32_t j = threadIdx.x >> 5; j < jn; j += BLOCK / 32) {
-        uint32_t pre[G + 1], st[G];
+        // run r covers chunk positions [pre[r], pre[r+1]); position e of run r is problem
+        // item dl[r] + e (dl[r] = run start - pre[r], precomputed once per bucket)
+        uint32_t pre[G + 1], dl[G];
         pre[0] = 0;
 #pragma unroll
         for (int r = 0; r < G; ++r) {
-            st[r] = (uint32_t)(i0 + r) * lv.L + sp[r][j];                // item index in the problem
+            dl[r] = (uint32_t)(i0 + r) * lv.L + sp[r][j] - pre[r];
             pre[r + 1] = pre[r] + sa[r][j];
         }
         const uint32_t total = pre[G], d0 = sl[j];
@@ -1296,10 +1298,10 @@ __global__ void __launch_bounds__(BLOCK) k_relocate_grouped(LevelDev lv)
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const uint32_t e = e0 + u * 32 + lane;
-                uint32_t base = st[0];
+                uint32_t base = dl[0];
 #pragma unroll
                 for (int k = 1; k < G; ++k)
-                    if (e >= pre[k]) base = st[k] - pre[k];
+                    if (e >= pre[k]) base = dl[k];
                 q[u] = base + e;
                 if (e < total) y[u] = src[q[u]];
             }

@@ -100,6 +100,13 @@ __device__ __forceinline__ void reg_sort(T (&x)[M])
 #define GBS_NARROW_SPLIT 1   // merge chains after the first search a window of H + 1 for their split
 #endif
 
+#ifndef GBS_REV_B
+// Shared-memory merge levels keep the B run of every pair stored descending (a bitonic
+// pair): a merge pointer that runs past the end of its run then walks down the other
+// run from its far end, so no end-of-run checks are needed (see merge_thread)
+#define GBS_REV_B 1
+#endif
+
 #ifndef GBS_PAD_SHIFT
 #define GBS_PAD_SHIFT 0   // 0 = one pad slot per ITEMS
 #endif
@@ -143,23 +150,56 @@ struct CtaSort {
     // the same, knowing the split lies in [lo, hi]
     static __device__ __forceinline__ int split_in(const T* sm, int a0, int w, int diag, int lo, int hi)
     {
-        const int b0 = a0 + w;
+        // B[diag-1-mid] sits at b0 + diag - 1 - mid, or (B descending, GBS_REV_B) at
+        // a0 + 2w - 1 - (diag - 1 - mid) = bt + mid
+        const int b0 = a0 + w, bt = a0 + 2 * w - diag;
         while (lo < hi) {
             const int mid = (lo + hi) >> 1;
-            if (sm[phys(a0 + mid)] <= sm[phys(b0 + diag - 1 - mid)]) lo = mid + 1;
+            const int bpos = GBS_REV_B ? bt + mid : b0 + diag - 1 - mid;
+            if (sm[phys(a0 + mid)] <= sm[phys(bpos)]) lo = mid + 1;
             else hi = mid;
         }
         return lo;
+    }
+
+    // Store the thread's ITEMS outputs [start, start+ITEMS), which belong to runs of
+    // length w: ascending, or mirrored inside the run when the run is the B of the next
+    // level's pair (odd run index, GBS_REV_B).  `rev` is warp-uniform once w >= 32 ITEMS.
+    // lg = log2(w / ITEMS): the run of thread t is t >> lg (start = t ITEMS).
+    template <int M>
+    static __device__ __forceinline__ void store_run(const T (&x)[M], T* sm, int start, int w, int lg)
+    {
+        const int q = (int)threadIdx.x >> lg;                 // run index
+        if (GBS_REV_B && (q & 1)) {
+            const int r0 = (q << lg) * ITEMS;                 // run start
+            const int e = 2 * r0 + w - ITEMS - start;         // mirrored block start
+#pragma unroll
+            for (int k = 0; k < ITEMS; ++k) sm[phys(e + k)] = x[ITEMS - 1 - k];
+        } else {
+#pragma unroll
+            for (int k = 0; k < ITEMS; ++k) sm[phys(start + k)] = x[k];
+        }
     }
 
     // The thread's ITEMS outputs [start, start+ITEMS) of the merge of the pair of
     // sorted runs (A = [base, base+w), B = [base+w, base+2w)) containing `start`,
     // produced by CHAINS independent merge-path chains of ITEMS/CHAINS outputs each,
     // interleaved for ILP (each step of a chain waits on one shared-memory load).
-    // Per chain only the A index is kept: B's index is (2 base + w + diag) - A index.
-    // An exhausted run reads as TMAX ("sticky sentinel"): for keys a tie between a
-    // real 0xFFFFFFFF and the sentinel outputs the same value; u64 items never equal
-    // TMAX.  Ties take A first, so the merge is stable.
+    // Ties take A first, so the merge is stable.
+    //
+    // GBS_REV_B: B is stored descending (B[j] at base + 2w - 1 - j).  Per chain only the
+    // A position ai is kept; the B head sits at ai + E - k after k outputs.  A pointer
+    // that passes the end of its run reads the other run from its far end (its largest
+    // remaining item), so every output is still the smallest remaining item and no
+    // end-of-run check is needed: the two pointers consume the remaining items from both
+    // ends and never cross within the thread's outputs.  The only items that can then be
+    // taken "from the wrong side" are equal to the true output: keys (values only) are
+    // unaffected, and 8-byte items (u64 composites, pairs as key<<32|position) are
+    // distinct.
+    //
+    // Otherwise (B ascending): B's index is (2 base + w + diag) - A index, and an
+    // exhausted run reads as TMAX ("sticky sentinel"), with a warp-uniform fast path when
+    // no lane can exhaust a run inside its outputs.
     template <int M>
     static __device__ __forceinline__ void merge_thread(T (&x)[M], const T* sm, int start, int w)
     {
@@ -180,10 +220,33 @@ struct CtaSort {
             sp = c == 0 || !GBS_NARROW_SPLIT ? split(sm, base, w, diag)
                                              : split_in(sm, base, w, diag, max(sp, diag - w), min(sp + H, min(diag, w)));
             ai[c] = base + sp;
-            cb[c] = 2 * base + w + diag;              // bi = cb - ai
-            const int bi = cb[c] - ai[c];
-            a[c] = ai[c] < aEnd ? sm[phys(ai[c])] : TMAX;
-            b[c] = bi < bEnd ? sm[phys(bi)] : TMAX;
+            if (GBS_REV_B) {
+                cb[c] = bEnd - 1 - base - diag;           // E: B head = ai + E - k
+                a[c] = sm[phys(ai[c])];
+                b[c] = sm[phys(ai[c] + cb[c])];
+            } else {
+                cb[c] = 2 * base + w + diag;              // bi = cb - ai
+                const int bi = cb[c] - ai[c];
+                a[c] = ai[c] < aEnd ? sm[phys(ai[c])] : TMAX;
+                b[c] = bi < bEnd ? sm[phys(bi)] : TMAX;
+            }
+        }
+        if (GBS_REV_B) {
+#pragma unroll
+            for (int k = 0; k < H; ++k) {
+#pragma unroll
+                for (int c = 0; c < CHAINS; ++c) {
+                    const bool t = a[c] <= b[c];
+                    x[c * H + k] = t ? a[c] : b[c];
+                    const int bnext = ai[c] + cb[c] - (k + 1);
+                    ai[c] += t ? 1 : 0;
+                    const int nidx = t ? ai[c] : bnext;
+                    const T v = sm[phys_fma(nidx)];
+                    a[c] = t ? v : a[c];
+                    b[c] = t ? b[c] : v;
+                }
+            }
+            return;
         }
         // Fast path (warp-uniform): no lane can exhaust a run inside its H outputs, so
         // the end-of-run checks (3 ALU-pipe ops per step) are dropped.
@@ -325,18 +388,32 @@ struct CtaSort {
             const int p = t + k * BLOCK;
             x[k] = p < valid ? src[p] : TMAX;
         }
+        // odd runs of R stored mirrored (GBS_REV_B): the B of each first-level pair
 #pragma unroll
-        for (int k = 0; k < ITEMS; ++k) sm[phys(t + k * BLOCK)] = x[k];
+        for (int k = 0; k < ITEMS; ++k) {
+            const int p = t + k * BLOCK;
+            const int r0 = p & ~(R - 1);
+            sm[phys(GBS_REV_B && (p & R) && R < TILE ? 2 * r0 + R - 1 - p : p)] = x[k];
+        }
         __syncthreads();
         const int start = t * ITEMS;
         const int wspan0 = (t >> 5) * WARP_SPAN;
+        int lg = __ffs(R / ITEMS) - 1;                   // log2(w / ITEMS)
 #pragma unroll 1
-        for (int w = R; w < TILE; w *= 2) {
+        for (int w = R; w < TILE; w *= 2, ++lg) {
             const bool intra = 2 * w <= WARP_SPAN;
             const bool active = intra ? (wspan0 < valid) : (start < valid);
             if (active) merge_thread(x, sm, start, w);
             if (intra) __syncwarp(); else __syncthreads();
-            if (active) {
+            if (GBS_REV_B) {
+                // every position is rewritten (the layout of the sentinel tail changes
+                // with the run parity); idle threads' outputs are all sentinels
+                if (!active) {
+#pragma unroll
+                    for (int k = 0; k < ITEMS; ++k) x[k] = TMAX;
+                }
+                store_run(x, sm, start, 2 * w, lg + 1);
+            } else if (active) {
 #pragma unroll
                 for (int k = 0; k < ITEMS; ++k) sm[phys(start + k)] = x[k];
             }
@@ -368,11 +445,11 @@ struct CtaSort {
             if constexpr (SHFL_LEVELS > 0) warp_bitonic(x);
         }
         const int start = t * ITEMS;
+        int lg = SHFL_LEVELS;                            // log2(w / ITEMS)
 #pragma unroll 1
-        for (int w = ITEMS << SHFL_LEVELS; w < TILE; w *= 2) {
+        for (int w = ITEMS << SHFL_LEVELS; w < TILE; w *= 2, ++lg) {
             const bool intra = 2 * w <= WARP_SPAN;
-#pragma unroll
-            for (int k = 0; k < ITEMS; ++k) sm[phys(start + k)] = x[k];
+            store_run(x, sm, start, w, lg);
             if (intra) __syncwarp(); else __syncthreads();
             const bool active = intra ? (wspan0 < valid) : (start < valid);
             if (active) merge_thread(x, sm, start, w);

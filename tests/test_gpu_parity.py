@@ -107,6 +107,29 @@ def test_stage_parity(dev, cfg, n, dist):
     assert np.array_equal(view(lay["relocated"], n, np.uint32), tr["relocated"])
 
 
+@pytest.mark.parametrize("cfg,n", [(None, 1 << 25), (None, 3 * (1 << 20) + 17), ((4096, 256), 500_000),
+                                   ((1 << 16, 512), 3_000_017), ((2048, 64), (1 << 20) + 3),
+                                   ((32768, 4096), 7 * (1 << 20) + 5)])
+@pytest.mark.parametrize("dist", ["uniform", "zero", "det_duplicates", "sorted"])
+def test_step4_splitter_selection(dev, cfg, n, dist):
+    """Step 4 as a merge tree with selection (R22; every plan here has more
+    than one tile of samples, some an odd number of sample runs): the splitters the
+    production path selects (stop after Step 6, not the full-merge stage-parity form of
+    stop 4/5) equal the oracle's g_k = sorted[(k+1)m - 1], and so do the counts a."""
+    keys = gi.generate(dist, n, seed=11)
+    pl = plan(n, TILE_KEYS, cfg)
+    _, _, tr = oracle.gbs_sort(keys, plan=pl, trace=True)
+    m, s = tr["a"].shape
+    assert m * s > (1 << 14)
+    lay = gbs.debug_layout(n, cfg=cfg)
+    ws = torch.zeros(gbs.workspace_size(n, cfg=cfg), dtype=torch.uint8, device=dev)
+    gpu_sort(keys, dev, cfg=cfg, stop=6, ws=ws)
+    spl = ws[lay["splitters"]:lay["splitters"] + 8 * s].cpu().numpy().view(np.uint64)
+    assert np.array_equal(spl, tr["splitters"])
+    a = ws[lay["a"]:lay["a"] + 4 * m * s].cpu().numpy().view(np.uint32).reshape(m, s)
+    assert np.array_equal(a, tr["a"])
+
+
 @pytest.mark.parametrize("n", [2, 1000, 16384, 16385, 65536, 1 << 20, 2_000_003])
 @pytest.mark.parametrize("dist", ["uniform", "zero", "det_duplicates", "sorted", "gaussian"])
 def test_pairs_stable(dev, n, dist):

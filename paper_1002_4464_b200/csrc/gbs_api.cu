@@ -158,13 +158,19 @@ struct Node {
 // Step 9 mid tier: 5/8 of the full tile; keys on 512 threads x 40 (64 registers, 2 CTAs
 // per SM), 8-byte items on 1024 x 10 (20 u64 per thread would spill)
 #ifndef GBS_MID_KEYS_ITEMS
-#define GBS_MID_KEYS_ITEMS 48   // 512 x 48: buckets just above half a tile (measured: 40 -> 48 +1.4% at C2)
+#define GBS_MID_KEYS_ITEMS 48   // 512 x 48: top-level buckets just above half a tile (measured: 40 -> 48 +1.4% at C2)
+#endif
+#ifndef GBS_MID_KEYS_ITEMS_NESTED
+#define GBS_MID_KEYS_ITEMS_NESTED 40   // nested levels (wider bucket spread): 512 x 40 (measured: 48 is 8% slower at 2^27)
 #endif
 #define MID_BLOCK_OF(KIND) ((KIND) == KIND_KEYS ? 512 : 1024)
 #define MID_ITEMS_OF(KIND) ((KIND) == KIND_KEYS ? GBS_MID_KEYS_ITEMS : GBS_WIDE_ITEMS * 5 / 8)
-static constexpr uint32_t mid_cap(int kind)
+// the mid tier's capacity for a node (keys: 48 items per thread at the top level, 40 in
+// nested levels)
+static uint32_t mid_cap(int kind, uint32_t B)
 {
-    return kind == KIND_KEYS ? 512u * GBS_MID_KEYS_ITEMS : 1024u * (GBS_WIDE_ITEMS * 5 / 8);
+    if (kind != KIND_KEYS) return 1024u * (GBS_WIDE_ITEMS * 5 / 8);
+    return 512u * (B == 1 ? GBS_MID_KEYS_ITEMS : GBS_MID_KEYS_ITEMS_NESTED);
 }
 static bool split_step9(int kind, const Node& nd)
 {
@@ -176,7 +182,7 @@ static int step9_launches(int kind, const Node& nd)
     if (!(GBS_SPLIT_STEP9_ON && split_step9(kind, nd))) return 1;
     // + the classification kernel (k_bucket_tiers)
     if (!GBS_MID_STEP9) return 3;
-    return nd.hi > mid_cap(kind) ? 4 : 3;
+    return nd.hi > mid_cap(kind, nd.B) ? 4 : 3;
 }
 
 struct Plan {
@@ -655,7 +661,7 @@ static gbs_status_t launch_step9(const LevelDev& lv, const Node& nd, char* ws, c
             const uint32_t count = nd.B * nd.s;
             uint32_t* lists = reinterpret_cast<uint32_t*>(ws + nd.o_tiers);
             uint32_t* lens = lists + 3 * (uint64_t)count;
-            const uint32_t cut1 = GBS_MID_STEP9 ? mid_cap(KIND) : TILE;
+            const uint32_t cut1 = GBS_MID_STEP9 ? mid_cap(KIND, nd.B) : TILE;
             GBS_CUDA(cudaMemsetAsync(lens, 0, 16, st));
             launch_k(k_bucket_tiers, (count + 255) / 256, 256, 0, st, lv, lists, lens, TILE / 2, cut1);
             GBS_LAUNCHED();
@@ -688,7 +694,14 @@ static gbs_status_t launch_step9(const LevelDev& lv, const Node& nd, char* ws, c
                     }
                     GBS_LAUNCHED();
                 }
-                launch_seg_t<KIND, MID_BLOCK_OF(KIND), MID_ITEMS_OF(KIND), MODE>(t1, count, s12);
+                bool nested_mid = false;
+                if constexpr (KIND == KIND_KEYS) {
+                    if (nd.B != 1) {
+                        launch_seg_t<KIND, MID_BLOCK_OF(KIND), GBS_MID_KEYS_ITEMS_NESTED, MODE>(t1, count, s12);
+                        nested_mid = true;
+                    }
+                }
+                if (!nested_mid) launch_seg_t<KIND, MID_BLOCK_OF(KIND), MID_ITEMS_OF(KIND), MODE>(t1, count, s12);
                 GBS_LAUNCHED();
             } else {
                 if constexpr (KIND == KIND_KEYS) launch_seg_t<KIND, GBS_BIG_KEYS, MODE>(t1, count, s12);

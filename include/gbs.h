@@ -61,6 +61,24 @@ gbs_status_t gbs_sort_pairs_workspace_size(size_t n, size_t* bytes);
 gbs_status_t gbs_sort_pairs(uint32_t* d_keys, uint32_t* d_vals, size_t n, void* d_ws,
                             size_t ws_bytes, gbs_stream_t stream);
 
+/* Key types beyond unsigned 32-bit (the paper never fixes the item
+ * type, R1).  Signed int32 and IEEE-754 binary32 keys are sorted as u32 keys after
+ * an order-preserving bijection of their bits, applied in place before the sort and
+ * inverted after it (two streaming kernels, both on `stream`):
+ *   GBS_KEY_I32: flip the sign bit;
+ *   GBS_KEY_F32: negative (sign set) -> flip every bit, otherwise flip the sign bit.
+ * Float order is the IEEE-754 totalOrder of the bit patterns: -NaN < -inf < ... < -0 <
+ * +0 < ... < +inf < +NaN (so -0 sorts before +0, NaNs go to the ends by sign).
+ * GBS_KEY_U32 is gbs_sort_keys / gbs_sort_pairs.  Every argument is validated before the
+ * first kernel; d_keys must be 4-byte aligned; workspace as gbs_sort_keys_workspace_size
+ * (keys) or gbs_sort_pairs_workspace_size (pairs).  Pairs: stable by key, as
+ * gbs_sort_pairs.  On GBS_ERROR_CUDA the buffers' contents are unspecified. */
+typedef enum { GBS_KEY_U32 = 0, GBS_KEY_I32 = 1, GBS_KEY_F32 = 2 } gbs_key_type_t;
+gbs_status_t gbs_sort_keys_typed(void* d_keys, size_t n, int key_type, void* d_ws, size_t ws_bytes,
+                                 gbs_stream_t stream);
+gbs_status_t gbs_sort_pairs_typed(void* d_keys, uint32_t* d_vals, size_t n, int key_type, void* d_ws,
+                                  size_t ws_bytes, gbs_stream_t stream);
+
 /* End to end from HOST buffers: copy h_keys (pinned host, n keys) to d_keys, sort,
  * copy back to h_keys; all three enqueued on `stream` (H2D + sort + D2H). */
 gbs_status_t gbs_sort_keys_host(uint32_t* h_keys, size_t n, uint32_t* d_keys, void* d_ws,

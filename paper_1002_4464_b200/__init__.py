@@ -65,6 +65,8 @@ def lib():
             "gbs_sort_keys": [p, sz, p, sz, p],
             "gbs_sort_pairs": [p, p, sz, p, sz, p],
             "gbs_sort_keys_host": [p, sz, p, p, sz, p],
+            "gbs_sort_keys_typed": [p, sz, C.c_int, p, sz, p],
+            "gbs_sort_pairs_typed": [p, p, sz, C.c_int, p, sz, p],
             "gbs_plan": [sz, C.c_int, C.POINTER(Config), C.POINTER(PlanT)],
             "gbs_workspace_size_ex": [sz, C.c_int, C.POINTER(Config), C.POINTER(sz)],
             "gbs_debug_layout": [sz, C.c_int, C.POINTER(Config), C.POINTER(LayoutT)],
@@ -208,6 +210,45 @@ def sort_pairs(keys, vals, ws: Workspace | None = None, stream=None):
     need = workspace_size(n, pairs=True)
     wp, wb = _ws_for(need, ws, keys.device)
     _check(lib().gbs_sort_pairs(C.c_void_p(kp), C.c_void_p(vp), n, wp, wb, _stream(stream)))
+    return keys, vals
+
+
+KEY_TYPES = {"uint32": 0, "int32": 1, "float32": 2}
+
+
+def _key_type(t, key_type):
+    torch = _torch()
+    if key_type is None:
+        key_type = {torch.uint32: "uint32", torch.int32: "int32", torch.float32: "float32"}.get(t.dtype)
+        if key_type is None:
+            raise GbsError("keys must be uint32, int32 or float32")
+    if key_type not in KEY_TYPES:
+        raise GbsError(f"key_type must be one of {sorted(KEY_TYPES)}")
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or not t.is_contiguous() or t.element_size() != 4:
+        raise GbsError("keys must be a contiguous CUDA tensor of 4-byte elements")
+    return KEY_TYPES[key_type]
+
+
+def sort_keys_typed(keys, key_type=None, ws: Workspace | None = None, stream=None):
+    """Sort a CUDA tensor in place by its value as uint32, int32 or float32 (default: the
+    tensor's dtype; floats in IEEE-754 totalOrder, -0 before +0, NaNs at the ends by sign)."""
+    kt = _key_type(keys, key_type)
+    n = keys.numel()
+    wp, wb = _ws_for(workspace_size(n), ws, keys.device)
+    _check(lib().gbs_sort_keys_typed(C.c_void_p(keys.data_ptr()), n, kt, wp, wb, _stream(stream)))
+    return keys
+
+
+def sort_pairs_typed(keys, vals, key_type=None, ws: Workspace | None = None, stream=None):
+    """Stable (key, value) sort in place with uint32 / int32 / float32 keys (as sort_keys_typed)."""
+    kt = _key_type(keys, key_type)
+    n = keys.numel()
+    if vals.numel() != n:
+        raise GbsError("keys and vals must have the same length")
+    vp = _dev_ptr(vals, "vals")
+    wp, wb = _ws_for(workspace_size(n, pairs=True), ws, keys.device)
+    _check(lib().gbs_sort_pairs_typed(C.c_void_p(keys.data_ptr()), C.c_void_p(vp), n, kt, wp, wb,
+                                      _stream(stream)))
     return keys, vals
 
 

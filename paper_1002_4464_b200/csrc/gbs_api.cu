@@ -1115,6 +1115,51 @@ gbs_status_t gbs_sort_pairs(uint32_t* d_keys, uint32_t* d_vals, size_t n, void* 
     return run_sort(d_keys, d_vals, n, nullptr, 0, d_ws, ws_bytes, (cudaStream_t)stream);
 }
 
+// Typed keys: validate everything run_sort would (so nothing is enqueued on a bad call),
+// transform the keys in place, sort them as u32, transform back.
+static gbs_status_t run_sort_typed(void* keys, uint32_t* vals, size_t n, int type, void* ws, size_t ws_bytes,
+                                   cudaStream_t st)
+{
+    if (type < GBS_KEY_U32 || type > GBS_KEY_F32) return fail(GBS_ERROR_INVALID_VALUE, "key_type %d", type);
+    uint32_t* k = reinterpret_cast<uint32_t*>(keys);
+    if (type == GBS_KEY_U32 || n <= 1) return run_sort(k, vals, n, nullptr, 0, ws, ws_bytes, st);
+    Plan P;
+    gbs_status_t r = make_plan(n, vals ? KIND_PAIRS : KIND_KEYS, nullptr, P);
+    if (r) return r;
+    if (!k) return fail(GBS_ERROR_INVALID_VALUE, "d_keys is NULL");
+    if (((uintptr_t)k & 3) || (vals && ((uintptr_t)vals & 3)))
+        return fail(GBS_ERROR_INVALID_VALUE, "keys/values must be 4-byte aligned");
+    if (vals) {
+        const uintptr_t k0 = (uintptr_t)k, k1 = k0 + n * 4, v0 = (uintptr_t)vals, v1 = v0 + n * 4;
+        if (k0 < v1 && v0 < k1) return fail(GBS_ERROR_INVALID_VALUE, "keys and values overlap");
+    }
+    if (ws_bytes < P.ws) return fail(GBS_ERROR_WORKSPACE_TOO_SMALL, "workspace %zu < %zu bytes", ws_bytes, P.ws);
+    if (P.ws && (!ws || ((uintptr_t)ws & 255))) return fail(GBS_ERROR_INVALID_VALUE, "workspace NULL or not 256-byte aligned");
+    r = check_device();
+    if (r) return r;
+    const unsigned grid = num_sms() * 4;
+    launch_k(k_key_transform, grid, 256, 0, st, k, (uint64_t)n, type, 0);
+    GBS_CUDA(cudaGetLastError());
+    r = run_sort(k, vals, n, nullptr, 0, ws, ws_bytes, st);
+    if (r) return r;
+    launch_k(k_key_transform, grid, 256, 0, st, k, (uint64_t)n, type, 1);
+    GBS_CUDA(cudaGetLastError());
+    return GBS_SUCCESS;
+}
+
+gbs_status_t gbs_sort_keys_typed(void* d_keys, size_t n, int key_type, void* d_ws, size_t ws_bytes,
+                                 gbs_stream_t stream)
+{
+    return run_sort_typed(d_keys, nullptr, n, key_type, d_ws, ws_bytes, (cudaStream_t)stream);
+}
+
+gbs_status_t gbs_sort_pairs_typed(void* d_keys, uint32_t* d_vals, size_t n, int key_type, void* d_ws,
+                                  size_t ws_bytes, gbs_stream_t stream)
+{
+    if (n > 1 && !d_vals) return fail(GBS_ERROR_INVALID_VALUE, "d_vals is NULL");
+    return run_sort_typed(d_keys, d_vals, n, key_type, d_ws, ws_bytes, (cudaStream_t)stream);
+}
+
 gbs_status_t gbs_sort_ex(uint32_t* d_keys, uint32_t* d_vals, size_t n, const gbs_config_t* cfg, int stop_after_step,
                          void* d_ws, size_t ws_bytes, gbs_stream_t stream)
 {

@@ -1485,6 +1485,36 @@ __global__ void __launch_bounds__(BLOCK, 1) k_segment_sort_rare(LevelDev lv)
     }
 }
 
+// Typed keys (gbs_sort_keys_typed, NEXT-4): an order-preserving bijection of int32 /
+// binary32 bit patterns onto u32, in place (inverse = 1 undoes it).  int32: x ^ 2^31.
+// float: negatives (sign set) -> ~x, others -> x ^ 2^31; inverse: top bit set -> x ^ 2^31,
+// else ~x.  16-byte vectors when the buffer is 16-byte aligned.
+__device__ __forceinline__ uint32_t key_fwd(uint32_t x, int type)
+{
+    if (type == 1) return x ^ 0x80000000u;
+    return x ^ ((x >> 31) ? 0xFFFFFFFFu : 0x80000000u);
+}
+__device__ __forceinline__ uint32_t key_inv(uint32_t x, int type)
+{
+    if (type == 1) return x ^ 0x80000000u;
+    return x ^ ((x >> 31) ? 0x80000000u : 0xFFFFFFFFu);
+}
+__global__ void k_key_transform(uint32_t* k, uint64_t n, int type, int inverse)
+{
+    pdl_entry();
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (uint64_t)gridDim.x * blockDim.x;
+    const bool vec = ((uintptr_t)k & 15) == 0;
+    const uint64_t nv = vec ? n / 4 : 0;
+    uint4* k4 = reinterpret_cast<uint4*>(k);
+    for (uint64_t q = tid; q < nv; q += stride) {
+        uint4 v = k4[q];
+        if (inverse) { v.x = key_inv(v.x, type); v.y = key_inv(v.y, type); v.z = key_inv(v.z, type); v.w = key_inv(v.w, type); }
+        else { v.x = key_fwd(v.x, type); v.y = key_fwd(v.y, type); v.z = key_fwd(v.z, type); v.w = key_fwd(v.w, type); }
+        k4[q] = v;
+    }
+    for (uint64_t e = nv * 4 + tid; e < n; e += stride) k[e] = inverse ? key_inv(k[e], type) : key_fwd(k[e], type);
+}
+
 // Debug-only invariant checks (GBS_DEBUG_SYNC): *flag |= 1 if some problem's sorted
 // samples are out of order, |= 2 if some row of a does not sum to the sublist's
 // real item count (conservation).

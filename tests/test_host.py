@@ -79,6 +79,13 @@ def test_validation_before_device_work():
     # workspace too small is reported, not crashed on
     assert L.gbs_sort_keys(C.c_void_p(16), 1 << 20, C.c_void_p(256), 10, None) == 2
     assert L.gbs_sort_keys(None, 0, None, 0, None) == 0 and L.gbs_sort_keys(None, 1, None, 0, None) == 0
+    # typed keys: a bad key type, NULL keys, a short workspace -- all rejected before the
+    # in-place key transform is enqueued
+    assert L.gbs_sort_keys_typed(C.c_void_p(16), 100, 7, None, 0, None) == 1
+    assert L.gbs_sort_keys_typed(None, 100, 2, None, 0, None) == 1
+    assert L.gbs_sort_keys_typed(C.c_void_p(16), 1 << 20, 1, C.c_void_p(256), 10, None) == 2
+    assert L.gbs_sort_pairs_typed(C.c_void_p(16), None, 100, 2, None, 0, None) == 1
+    assert L.gbs_sort_keys_typed(None, 1, 2, None, 0, None) == 0
 
 
 def test_exchange_plan_against_direct_definition():

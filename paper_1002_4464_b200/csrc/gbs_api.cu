@@ -93,6 +93,9 @@ constexpr uint64_t SMALL_U64_TOTAL = 1u << 18;   // u64 levels up to this many s
 #ifndef GBS_PAIR_BELOW_D
 #define GBS_PAIR_BELOW_D 16                       // CTA-pair sublists when the one-tile d is below (0 = off)
 #endif
+#ifndef GBS_SMALL_N_KEYS
+#define GBS_SMALL_N_KEYS (1u << 17)   // keys problems up to this size use 2K sublists and buckets (0 = off)
+#endif
 #ifndef GBS_U64_MED_TOTAL
 #define GBS_U64_MED_TOTAL 0                       // ... and up to this many 8K tiles (0 = off; measured slower at C2/C3)
 #endif
@@ -240,6 +243,14 @@ static int build_node(Plan& P, int kind, uint32_t B, uint64_t N, uint32_t pad_ba
         if (kind == KIND_U64 && (uint64_t)B * N <= SMALL_U64_TOTAL) {
             for (uint32_t c = 2; c <= SMALL_TILE / D_MIN; c *= 2)
                 if (hi_bound(N, SMALL_TILE, c) <= SMALL_TILE) { s = c; break; }
+        }
+        // A small keys problem (a few big-tile sublists) is latency-bound the same way:
+        // 2K sublists and 2K buckets spread Steps 2 and 9 over many SMs (2^16: 0.119 ->
+        // 0.047 ms).  Up to 2^17 keys, where the samples still sort in one CTA; above,
+        // the larger Step 4 costs more than the spread saves (measured at 2^20, 2^21).
+        if (kind == KIND_KEYS && B == 1 && N <= GBS_SMALL_N_KEYS) {
+            for (uint32_t c = 2; c <= SMALL_TILE / D_MIN && !s; c *= 2)
+                if (hi_bound(N, SMALL_TILE, c) <= SMALL_TILE) s = c;
         }
         if (s) {
             L = SMALL_TILE;

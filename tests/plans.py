@@ -13,6 +13,8 @@ TILE_PAIRS = 1 << 14    # (key, value) pairs per CTA tile
 D_MIN = 8               # a single level needs d = L/s >= 8 (samples <= n/8)
 D_NEST = 32             # d of a level whose buckets need a nested level
 PAIR_BELOW_D = 16       # keys: sublists of two tiles (CTA pairs) when the one-tile d is below
+SMALL_TILE = 1 << 11    # the small CTA configuration's tile (the paper's 2K sublists)
+SMALL_N_KEYS = 1 << 17  # keys problems up to this size: 2K sublists and buckets (latency: more CTAs)
 
 
 def hi_bound(cap: int, L: int, s: int) -> int:
@@ -28,6 +30,13 @@ def plan(n: int, tile: int = TILE_KEYS, cfg=None):
     if cfg is not None and n > 1:          # explicit level-1 (L, s), e.g. the paper's
         levels.append(tuple(cfg))          # (2048, 64) of P:249-250
         cap = hi_bound(n, *cfg)
+    if not levels and tile == TILE_KEYS and tile < n <= SMALL_N_KEYS:
+        # small keys problem: 2K sublists when some s (d >= D_MIN) gives buckets of <= 2K
+        s = 2
+        while s <= SMALL_TILE // D_MIN:
+            if hi_bound(n, SMALL_TILE, s) <= SMALL_TILE:
+                return [(SMALL_TILE, s)]
+            s *= 2
     while cap > tile:
         L = tile
         chosen = None

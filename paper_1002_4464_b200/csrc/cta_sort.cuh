@@ -114,6 +114,11 @@ __device__ __forceinline__ void reg_sort(T (&x)[M])
 template <typename T, int BLOCK, int ITEMS, int CHAINS_ = 0, int PAD_ = GBS_PAD_SHIFT>
 struct CtaSort {
     static constexpr int TILE = BLOCK * ITEMS;
+    // A tile that is not a power of two (BLOCK not a power of two, e.g. 544 x 32) has a
+    // short last run at some levels; with B runs stored descending (GBS_REV_B) the merge
+    // handles it by clipping the pair's run lengths (la, lb), nothing else changes.
+    static constexpr bool POW2_TILE = (TILE & (TILE - 1)) == 0;
+    static_assert(POW2_TILE || GBS_REV_B, "non-power-of-two tiles need GBS_REV_B");
     static constexpr int LOG_ITEMS = Ctz<ITEMS>::value;   // log2(ITEMS) for a power of two
     static constexpr int WARP_SPAN = 32 * ITEMS;                  // items owned by one warp
     // Shared-memory layout: one pad slot every 2^PAD items.  PAD = ctz(ITEMS) (log2 for a
@@ -162,6 +167,18 @@ struct CtaSort {
         return lo;
     }
 
+    // REV layout with an explicit B top (first B item): B[j] at top - j
+    static __device__ __forceinline__ int split_top(const T* sm, int a0, int top, int diag, int lo, int hi)
+    {
+        const int bt = top - diag + 1;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (sm[phys(a0 + mid)] <= sm[phys(bt + mid)]) lo = mid + 1;
+            else hi = mid;
+        }
+        return lo;
+    }
+
     // Store the thread's ITEMS outputs [start, start+ITEMS), which belong to runs of
     // length w: ascending, or mirrored inside the run when the run is the B of the next
     // level's pair (odd run index, GBS_REV_B).  `rev` is warp-uniform once w >= 32 ITEMS.
@@ -172,7 +189,8 @@ struct CtaSort {
         const int q = (int)threadIdx.x >> lg;                 // run index
         if (GBS_REV_B && (q & 1)) {
             const int r0 = (q << lg) * ITEMS;                 // run start
-            const int e = 2 * r0 + w - ITEMS - start;         // mirrored block start
+            const int lr = POW2_TILE ? w : min(w, TILE - r0); // run length (the tile's last run may be short)
+            const int e = 2 * r0 + lr - ITEMS - start;        // mirrored block start
 #pragma unroll
             for (int k = 0; k < ITEMS; ++k) sm[phys(e + k)] = x[ITEMS - 1 - k];
         } else {
@@ -209,6 +227,11 @@ struct CtaSort {
         // taken on the thread index start / ITEMS)
         const int base = ((start / ITEMS) & ~(2 * (w / ITEMS) - 1)) * ITEMS;
         const int aEnd = base + w, bEnd = base + 2 * w;
+        // run lengths of the pair (a short last run only in a non-power-of-two tile: then
+        // B is empty or A is full); B's first item sits at `top` (B descending)
+        const int la = POW2_TILE ? w : min(w, TILE - base);
+        const int lb = POW2_TILE ? w : max(0, min(w, TILE - base - w));
+        const int top = base + la + lb - 1;
         int ai[CHAINS], cb[CHAINS];
         T a[CHAINS], b[CHAINS];
         // chain c's split lies in [split(c-1), split(c-1) + H]: H more outputs take at most
@@ -217,11 +240,15 @@ struct CtaSort {
 #pragma unroll
         for (int c = 0; c < CHAINS; ++c) {
             const int diag = start - base + c * H;
-            sp = c == 0 || !GBS_NARROW_SPLIT ? split(sm, base, w, diag)
-                                             : split_in(sm, base, w, diag, max(sp, diag - w), min(sp + H, min(diag, w)));
+            if (POW2_TILE)
+                sp = c == 0 || !GBS_NARROW_SPLIT ? split(sm, base, w, diag)
+                                                 : split_in(sm, base, w, diag, max(sp, diag - w), min(sp + H, min(diag, w)));
+            else
+                sp = split_top(sm, base, top, diag, c == 0 ? max(0, diag - lb) : max(sp, diag - lb),
+                               c == 0 ? min(diag, la) : min(sp + H, min(diag, la)));
             ai[c] = base + sp;
             if (GBS_REV_B) {
-                cb[c] = bEnd - 1 - base - diag;           // E: B head = ai + E - k
+                cb[c] = top - base - diag;                // E: B head = ai + E - k
                 a[c] = sm[phys(ai[c])];
                 b[c] = sm[phys(ai[c] + cb[c])];
             } else {
@@ -382,6 +409,7 @@ struct CtaSort {
     template <int M, typename Src>
     static __device__ __forceinline__ void sort_presorted(T (&x)[M], Src src, T* sm, int valid, int R)
     {
+        static_assert(POW2_TILE, "presorted runs: power-of-two tiles only");
         const int t = threadIdx.x;
 #pragma unroll
         for (int k = 0; k < ITEMS; ++k) {

@@ -160,20 +160,23 @@ struct Node {
 #endif
 // Step 9 mid tier: 5/8 of the full tile; keys on 512 threads x 40 (64 registers, 2 CTAs
 // per SM), 8-byte items on 1024 x 10 (20 u64 per thread would spill)
-#ifndef GBS_MID_KEYS_ITEMS
-#define GBS_MID_KEYS_ITEMS 48   // 512 x 48: top-level buckets just above half a tile (measured: 40 -> 48 +1.4% at C2)
+// Step 9 mid tier (buckets just above half a tile), keys: at the top level 544 x 32
+// (17408 keys: a non-power-of-two tile whose short last run the bitonic-pair merge clips;
+// power-of-two items keep the shuffle levels), in nested levels 512 x 40 (wider bucket
+// spread).  Buckets above the mid tier go to the full-tile tier.
+#ifndef GBS_MID_TOP_BLOCK
+#define GBS_MID_TOP_BLOCK 544
+#define GBS_MID_TOP_ITEMS 32
 #endif
 #ifndef GBS_MID_KEYS_ITEMS_NESTED
-#define GBS_MID_KEYS_ITEMS_NESTED 40   // nested levels (wider bucket spread): 512 x 40 (measured: 48 is 8% slower at 2^27)
+#define GBS_MID_KEYS_ITEMS_NESTED 40
 #endif
-#define MID_BLOCK_OF(KIND) ((KIND) == KIND_KEYS ? 512 : 1024)
-#define MID_ITEMS_OF(KIND) ((KIND) == KIND_KEYS ? GBS_MID_KEYS_ITEMS : GBS_WIDE_ITEMS * 5 / 8)
-// the mid tier's capacity for a node (keys: 48 items per thread at the top level, 40 in
-// nested levels)
+#define MID_BLOCK_OF(KIND) ((KIND) == KIND_KEYS ? GBS_MID_TOP_BLOCK : 1024)
+#define MID_ITEMS_OF(KIND) ((KIND) == KIND_KEYS ? GBS_MID_TOP_ITEMS : GBS_WIDE_ITEMS * 5 / 8)
 static uint32_t mid_cap(int kind, uint32_t B)
 {
     if (kind != KIND_KEYS) return 1024u * (GBS_WIDE_ITEMS * 5 / 8);
-    return 512u * (B == 1 ? GBS_MID_KEYS_ITEMS : GBS_MID_KEYS_ITEMS_NESTED);
+    return B == 1 ? (uint32_t)GBS_MID_TOP_BLOCK * GBS_MID_TOP_ITEMS : 512u * GBS_MID_KEYS_ITEMS_NESTED;
 }
 static bool split_step9(int kind, const Node& nd)
 {
@@ -708,7 +711,7 @@ static gbs_status_t launch_step9(const LevelDev& lv, const Node& nd, char* ws, c
                 bool nested_mid = false;
                 if constexpr (KIND == KIND_KEYS) {
                     if (nd.B != 1) {
-                        launch_seg_t<KIND, MID_BLOCK_OF(KIND), GBS_MID_KEYS_ITEMS_NESTED, MODE>(t1, count, s12);
+                        launch_seg_t<KIND, 512, GBS_MID_KEYS_ITEMS_NESTED, MODE>(t1, count, s12);
                         nested_mid = true;
                     }
                 }

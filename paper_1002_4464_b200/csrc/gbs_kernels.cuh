@@ -1377,7 +1377,7 @@ __host__ __device__ constexpr uint32_t gather_max_m(int kind) { return kind == K
 // walked segments with a work counter and register prefetch measured ~8% slower: the
 // shared register array across tile sizes costs more than the hidden load latency.)
 template <int KIND, int BLOCK, int ITEMS, int MODE>
-__global__ void __launch_bounds__(BLOCK, (BLOCK <= 512 ? 2 : 1)) k_segment_sort(LevelDev lv)
+__global__ void __launch_bounds__(BLOCK, (BLOCK <= 576 ? 2 : 1)) k_segment_sort(LevelDev lv)
 {
     pdl_entry();
     // the mid tier (ITEMS not a power of two) only sees sizes just above the small tier

@@ -178,6 +178,20 @@ static uint32_t mid_cap(int kind, uint32_t B)
     if (kind != KIND_KEYS) return 1024u * (GBS_WIDE_ITEMS * 5 / 8);
     return B == 1 ? (uint32_t)GBS_MID_TOP_BLOCK * GBS_MID_TOP_ITEMS : 512u * GBS_MID_KEYS_ITEMS_NESTED;
 }
+// The mid tiers of a node: keys at the top level have two, (C/2, 544 x 32] and
+// (544 x 32, 512 x 48] (few-bucket problems spread wider); everything else one.
+// cuts[0..2] are the tiers' upper bounds (an unused tier repeats the previous cut).
+#ifndef GBS_MID2_TOP_ITEMS
+#define GBS_MID2_TOP_ITEMS 48
+#endif
+static void tier_cuts(int kind, const Node& nd, uint32_t tile, uint32_t cuts[3])
+{
+    cuts[0] = tile / 2;
+    cuts[1] = GBS_MID_STEP9 ? mid_cap(kind, nd.B) : tile;
+    cuts[2] = cuts[1];
+    if (GBS_MID_STEP9 && kind == KIND_KEYS && nd.B == 1 && GBS_MID2_TOP_ITEMS > 0)
+        cuts[2] = std::max(cuts[1], 512u * GBS_MID2_TOP_ITEMS);
+}
 static bool split_step9(int kind, const Node& nd)
 {
     return !nd.bucket_small && nd.step9 < 0 && nd.hi > tile_of(kind) / 2;
@@ -188,7 +202,9 @@ static int step9_launches(int kind, const Node& nd)
     if (!(GBS_SPLIT_STEP9_ON && split_step9(kind, nd))) return 1;
     // + the classification kernel (k_bucket_tiers)
     if (!GBS_MID_STEP9) return 3;
-    return nd.hi > mid_cap(kind, nd.B) ? 4 : 3;
+    uint32_t cuts[3];
+    tier_cuts(kind, nd, tile_of(kind), cuts);
+    return 3 + (nd.hi > cuts[1] && cuts[2] > cuts[1] ? 1 : 0) + (nd.hi > cuts[2] ? 1 : 0);
 }
 
 struct Plan {
@@ -321,7 +337,7 @@ static int build_node(Plan& P, int kind, uint32_t B, uint64_t N, uint32_t pad_ba
         // buckets that may exceed half a tile: size tiers (see exec_kind)
         P.launches += step9_launches(kind, P.nodes[idx]);
         if (GBS_SPLIT_STEP9_ON && split_step9(kind, P.nodes[idx]))
-            P.nodes[idx].o_tiers = P.alloc(((uint64_t)B * s * 3 + 4) * 4);
+            P.nodes[idx].o_tiers = P.alloc(((uint64_t)B * s * 4 + 4) * 4);
         // fused Step 8+9 when the bucket's m run descriptors fit the staging area
         // (a production call; stop_after_step runs keep the explicit Step 8)
         // (keys only for now: the 16-item u64 / pair gather variants spill registers)
@@ -456,8 +472,15 @@ static void launch_rare_t(const LevelDev& lv, unsigned count, cudaStream_t st)
 {
     const size_t sm = Seg<KIND, BLOCK, ITEMS>::smem_bytes();
     static std::once_flag f;
-    std::call_once(f, [&] { set_smem(k_segment_sort_rare<KIND, BLOCK, ITEMS>, sm); });
-    launch_k(k_segment_sort_rare<KIND, BLOCK, ITEMS>, std::min<unsigned>(count, num_sms()), BLOCK, sm, st, lv);
+    static int occ = 1;
+    std::call_once(f, [&] {
+        set_smem(k_segment_sort_rare<KIND, BLOCK, ITEMS>, sm);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_segment_sort_rare<KIND, BLOCK, ITEMS>, BLOCK, sm) !=
+                cudaSuccess || occ < 1)
+            occ = 1;
+    });
+    launch_k(k_segment_sort_rare<KIND, BLOCK, ITEMS>, std::min<unsigned>(count, num_sms() * (unsigned)occ), BLOCK, sm,
+             st, lv);
 }
 
 // Step 2 on CTA pairs: persistent clusters of two (one CTA per SM)
@@ -578,14 +601,14 @@ static uint32_t num_sms()
 // step (fork/join through events, so the call stays ordered on the caller's stream;
 // capturable into a CUDA graph).  Shared by concurrent calls: that only serialises the
 // side work, the dependencies stay per call.
-static cudaStream_t side_stream(int k = 0)   // k: 0 = Step 9 tiers, 1 = H2D, 2 = D2H
+static cudaStream_t side_stream(int k = 0)   // k: 0 = Step 9 tiers, 1 = H2D, 2 = D2H, 3 = more Step 9 tiers
 {
     static std::mutex mu;
-    static cudaStream_t ss[64][3] = {};
+    static cudaStream_t ss[64][4] = {};
     int dev = 0;
     cudaGetDevice(&dev);
     std::lock_guard<std::mutex> g(mu);
-    if (dev < 0 || dev >= 64 || k < 0 || k > 2) return nullptr;
+    if (dev < 0 || dev >= 64 || k < 0 || k > 3) return nullptr;
     if (!ss[dev][k] && cudaStreamCreateWithFlags(&ss[dev][k], cudaStreamNonBlocking) != cudaSuccess) ss[dev][k] = nullptr;
     return ss[dev][k];
 }
@@ -674,61 +697,74 @@ static gbs_status_t launch_step9(const LevelDev& lv, const Node& nd, char* ws, c
             // k_bucket_tiers).
             const uint32_t count = nd.B * nd.s;
             uint32_t* lists = reinterpret_cast<uint32_t*>(ws + nd.o_tiers);
-            uint32_t* lens = lists + 3 * (uint64_t)count;
-            const uint32_t cut1 = GBS_MID_STEP9 ? mid_cap(KIND, nd.B) : TILE;
+            uint32_t* lens = lists + 4 * (uint64_t)count;
+            uint32_t cuts[3];
+            tier_cuts(KIND, nd, TILE, cuts);
             GBS_CUDA(cudaMemsetAsync(lens, 0, 16, st));
-            launch_k(k_bucket_tiers, (count + 255) / 256, 256, 0, st, lv, lists, lens, TILE / 2, cut1);
+            launch_k(k_bucket_tiers, (count + 255) / 256, 256, 0, st, lv, lists, lens, cuts[0], cuts[1], cuts[2]);
             GBS_LAUNCHED();
-            LevelDev t0 = lv, t1 = lv, t2 = lv;
-            t0.tier_list = lists;
-            t0.tier_len = lens;
-            t1.tier_list = lists + count;
-            t1.tier_len = lens + 1;
-            t2.tier_list = lists + 2 * (uint64_t)count;
-            t2.tier_len = lens + 2;
+            LevelDev tl[4];
+            for (int q = 0; q < 4; ++q) {
+                tl[q] = lv;
+                tl[q].tier_list = lists + q * (uint64_t)count;
+                tl[q].tier_len = lens + q;
+            }
             // The tiers run concurrently: the larger tiers (few CTAs, each a full-tile
             // sort) on the side stream, so they are not a serial tail after tier 0.
-            cudaStream_t ss = side_stream();
-            cudaEvent_t fork = nullptr, join = nullptr;
-            if (ss) {
+            // (tier 1 on one side stream; tiers 2 and 3 -- usually empty -- on another)
+            cudaStream_t ss = side_stream(), ss2 = side_stream(3);
+            cudaEvent_t fork = nullptr, join = nullptr, join2 = nullptr;
+            if (ss && ss2) {
                 GBS_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
                 GBS_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+                GBS_CUDA(cudaEventCreateWithFlags(&join2, cudaEventDisableTiming));
                 GBS_CUDA(cudaEventRecord(fork, st));
                 GBS_CUDA(cudaStreamWaitEvent(ss, fork, 0));
+                GBS_CUDA(cudaStreamWaitEvent(ss2, fork, 0));
+            } else {
+                ss = ss2 = nullptr;
             }
-            cudaStream_t s12 = ss ? ss : st;
+            cudaStream_t s12 = ss ? ss : st, s23 = ss2 ? ss2 : st;
             if (GBS_MID_STEP9) {
-                if (nd.hi > cut1) {
+                if (nd.hi > cuts[2]) {   // the full tile
                     if constexpr (MODE == MODE_BUCKET && GBS_RARE_PERSIST) {
-                        if constexpr (KIND == KIND_KEYS) launch_rare_t<KIND, GBS_BIG_KEYS>(t2, count, s12);
-                        else launch_rare_t<KIND, GBS_BIG_WIDE>(t2, count, s12);
+                        if constexpr (KIND == KIND_KEYS) launch_rare_t<KIND, GBS_BIG_KEYS>(tl[3], count, s23);
+                        else launch_rare_t<KIND, GBS_BIG_WIDE>(tl[3], count, s23);
                     } else {
-                        if constexpr (KIND == KIND_KEYS) launch_seg_t<KIND, GBS_BIG_KEYS, MODE>(t2, count, s12);
-                        else launch_seg_t<KIND, GBS_BIG_WIDE, MODE>(t2, count, s12);
+                        if constexpr (KIND == KIND_KEYS) launch_seg_t<KIND, GBS_BIG_KEYS, MODE>(tl[3], count, s23);
+                        else launch_seg_t<KIND, GBS_BIG_WIDE, MODE>(tl[3], count, s23);
                     }
                     GBS_LAUNCHED();
                 }
-                bool nested_mid = false;
+                bool mid_done = false;
                 if constexpr (KIND == KIND_KEYS) {
                     if (nd.B != 1) {
-                        launch_seg_t<KIND, 512, GBS_MID_KEYS_ITEMS_NESTED, MODE>(t1, count, s12);
-                        nested_mid = true;
+                        launch_seg_t<KIND, 512, GBS_MID_KEYS_ITEMS_NESTED, MODE>(tl[1], count, s12);
+                        mid_done = true;
+                    } else if (nd.hi > cuts[1] && cuts[2] > cuts[1]) {
+                        // the second mid tier on persistent CTAs (usually few buckets)
+                        if constexpr (MODE == MODE_BUCKET) launch_rare_t<KIND, 512, GBS_MID2_TOP_ITEMS>(tl[2], count, s23);
+                        else launch_seg_t<KIND, 512, GBS_MID2_TOP_ITEMS, MODE>(tl[2], count, s23);
+                        GBS_LAUNCHED();
                     }
                 }
-                if (!nested_mid) launch_seg_t<KIND, MID_BLOCK_OF(KIND), MID_ITEMS_OF(KIND), MODE>(t1, count, s12);
+                if (!mid_done) launch_seg_t<KIND, MID_BLOCK_OF(KIND), MID_ITEMS_OF(KIND), MODE>(tl[1], count, s12);
                 GBS_LAUNCHED();
-            } else {
-                if constexpr (KIND == KIND_KEYS) launch_seg_t<KIND, GBS_BIG_KEYS, MODE>(t1, count, s12);
-                else launch_seg_t<KIND, GBS_BIG_WIDE, MODE>(t1, count, s12);
+            } else {   // no mid tier: (C/2, C] on the full tile
+                if constexpr (KIND == KIND_KEYS) launch_seg_t<KIND, GBS_BIG_KEYS, MODE>(tl[1], count, s12);
+                else launch_seg_t<KIND, GBS_BIG_WIDE, MODE>(tl[1], count, s12);
                 GBS_LAUNCHED();
             }
-            launch_seg_t<KIND, 512, ITEMS, MODE>(t0, count, st);
+            launch_seg_t<KIND, 512, ITEMS, MODE>(tl[0], count, st);
             GBS_LAUNCHED();
             if (ss) {
                 GBS_CUDA(cudaEventRecord(join, ss));
+                GBS_CUDA(cudaEventRecord(join2, ss2));
                 GBS_CUDA(cudaStreamWaitEvent(st, join, 0));
+                GBS_CUDA(cudaStreamWaitEvent(st, join2, 0));
                 cudaEventDestroy(fork);
                 cudaEventDestroy(join);
+                cudaEventDestroy(join2);
             }
         } else {
             launch_seg<KIND, MODE>(lv, nd.bucket_small, nd.B * nd.s, st);

@@ -1327,10 +1327,11 @@ __global__ void __launch_bounds__(BLOCK) k_relocate_grouped(LevelDev lv)
 // of a tier read neighbouring runs.  The output never depends on the list order: each
 // bucket is sorted on its own.
 __global__ void __launch_bounds__(256) k_bucket_tiers(LevelDev lv, uint32_t* lists, uint32_t* lens, uint32_t cut0,
-                                                      uint32_t cut1)
+                                                      uint32_t cut1, uint32_t cut2)
 {
     pdl_entry();
-    __shared__ uint32_t wcnt[3][8], wbase[3][8];
+    constexpr int NT = 4;   // tiers: (0, cut0], (cut0, cut1], (cut1, cut2], > cut2
+    __shared__ uint32_t wcnt[NT][8], wbase[NT][8];
     const uint32_t count = lv.B * lv.s;
     const uint32_t idx = blockIdx.x * 256 + threadIdx.x;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -1339,17 +1340,18 @@ __global__ void __launch_bounds__(256) k_bucket_tiers(LevelDev lv, uint32_t* lis
         uint64_t off;
         int v;
         segment_of<MODE_BUCKET>(lv, idx, off, v);
-        if (v > 0) t = (uint32_t)v <= cut0 ? 0 : ((uint32_t)v <= cut1 ? 1 : 2);
+        const uint32_t u = (uint32_t)v;
+        if (v > 0) t = u <= cut0 ? 0 : (u <= cut1 ? 1 : (u <= cut2 ? 2 : 3));
     }
     uint32_t mine = 0;
 #pragma unroll
-    for (int q = 0; q < 3; ++q) {
+    for (int q = 0; q < NT; ++q) {
         const uint32_t mask = __ballot_sync(0xffffffffu, t == q);
         if (lane == 0) wcnt[q][w] = __popc(mask);
         if (t == q) mine = __popc(mask & ((1u << lane) - 1u));
     }
     __syncthreads();
-    if (threadIdx.x < 3) {
+    if (threadIdx.x < NT) {
         const int q = threadIdx.x;
         uint32_t tot = 0;
         for (int k = 0; k < 8; ++k) { wbase[q][k] = tot; tot += wcnt[q][k]; }
@@ -1470,7 +1472,7 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK <= 576 ? 2 : 1)) k_segment_sort(
 // tier then costs one wave of CTAs that exit at once instead of one CTA per bucket slot
 // (whose 133 KB of shared memory each would block the concurrent small tier's CTAs).
 template <int KIND, int BLOCK, int ITEMS>
-__global__ void __launch_bounds__(BLOCK, 1) k_segment_sort_rare(LevelDev lv)
+__global__ void __launch_bounds__(BLOCK, (BLOCK <= 576 ? 2 : 1)) k_segment_sort_rare(LevelDev lv)
 {
     pdl_entry();
     using A = Adapt<KIND, BLOCK, ITEMS, GBS_ADAPT_DEPTH>;

@@ -103,7 +103,10 @@ constexpr uint32_t MED_TILE_U64 = 8192;
 constexpr uint32_t D_MIN = 8;              // single level needs d >= 8
 constexpr uint32_t D_NEST = 32;            // d of a level with a nested Step 9
 constexpr uint32_t MAX_S = 4096;           // shared-memory limit of Steps 6 and 8
-constexpr int IDX_BLOCK = 512;             // Steps 6 and 8 CTA size
+#ifndef GBS_IDX_BLOCK
+#define GBS_IDX_BLOCK 512
+#endif
+constexpr int IDX_BLOCK = GBS_IDX_BLOCK;   // Steps 6 and 8 CTA size
 
 static constexpr uint32_t tile_of_c(int kind) { return kind == KIND_KEYS ? TILE_KEYS : (kind == KIND_PAIRS ? TILE_PAIRS : TILE_U64); }
 static uint32_t tile_of(int kind) { return tile_of_c(kind); }

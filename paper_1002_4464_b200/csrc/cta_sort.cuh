@@ -191,11 +191,15 @@ struct CtaSort {
             const int r0 = (q << lg) * ITEMS;                 // run start
             const int lr = POW2_TILE ? w : min(w, TILE - r0); // run length (the tile's last run may be short)
             const int e = 2 * r0 + lr - ITEMS - start;        // mirrored block start
+            // e and start are multiples of ITEMS, hence of the pad group 2^PAD, so
+            // phys(e + k) = phys(e) + k + (k >> PAD): one address, constant offsets
+            const int pe = phys(e);
 #pragma unroll
-            for (int k = 0; k < ITEMS; ++k) sm[phys(e + k)] = x[ITEMS - 1 - k];
+            for (int k = 0; k < ITEMS; ++k) sm[pe + k + (k >> PAD)] = x[ITEMS - 1 - k];
         } else {
+            const int ps = phys(start);
 #pragma unroll
-            for (int k = 0; k < ITEMS; ++k) sm[phys(start + k)] = x[k];
+            for (int k = 0; k < ITEMS; ++k) sm[ps + k + (k >> PAD)] = x[k];
         }
     }
 

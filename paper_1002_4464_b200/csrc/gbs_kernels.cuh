@@ -264,7 +264,18 @@ struct Seg {
         const T* sm = reinterpret_cast<const T*>(smem);
         if constexpr (KIND == KIND_KEYS) {
             uint32_t* d = reinterpret_cast<uint32_t*>(dst) + dst_off;
-            for (int p = threadIdx.x; p < v; p += BLOCK) d[p] = (uint32_t)sm[CS::phys(p)];
+            if constexpr (BLOCK % (1 << CS::PAD) == 0) {
+                // position tid + k BLOCK sits at phys(tid) + k (BLOCK + BLOCK >> PAD): one
+                // address, constant offsets (BLOCK is a multiple of the pad group)
+                const int t = threadIdx.x;
+                const T* s0 = sm + CS::phys(t);
+                uint32_t* d0 = d + t;
+#pragma unroll
+                for (int k = 0; k < ITEMS; ++k)
+                    if (t + k * BLOCK < v) d0[k * BLOCK] = (uint32_t)s0[k * (BLOCK + (BLOCK >> CS::PAD))];
+            } else {
+                for (int p = threadIdx.x; p < v; p += BLOCK) d[p] = (uint32_t)sm[CS::phys(p)];
+            }
         } else if constexpr (KIND == KIND_PAIRS) {
             const uint32_t* vsm = vsm_of(smem);
             uint32_t* d = reinterpret_cast<uint32_t*>(dst) + dst_off;

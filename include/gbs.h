@@ -20,7 +20,11 @@
  *     throws; gbs_last_error() holds a thread-local message for the last failure.
  *   - The result is bit-identical across runs and streams (deterministic: no
  *     atomics decide any output position).
- *   - Calls on distinct buffers/workspaces/streams may run concurrently.
+ *   - Calls on distinct buffers/workspaces/streams may run concurrently.  Inside a call,
+ *     Step 9's size tiers and the host-buffer copies run on side streams shared by all
+ *     calls on a device (forked from and joined back into `stream` with events), so a
+ *     call may be captured into a CUDA graph, but no other call on the same device may
+ *     be enqueued while that capture is open.
  *   - Limits: n <= 2^31 items per call (32-bit tags, R10).
  */
 #ifndef GBS_H_
@@ -80,9 +84,18 @@ gbs_status_t gbs_sort_pairs_typed(void* d_keys, uint32_t* d_vals, size_t n, int 
                                   size_t ws_bytes, gbs_stream_t stream);
 
 /* End to end from HOST buffers: copy h_keys (pinned host, n keys) to d_keys, sort,
- * copy back to h_keys; all three enqueued on `stream` (H2D + sort + D2H). */
+ * copy back to h_keys; all three enqueued on `stream` (H2D + sort + D2H).  Large inputs
+ * are pipelined: the H2D copy is chunked by sublists so Step 2 sorts each chunk as it
+ * lands, and (one-level plans) the final output is copied back bucket group by bucket
+ * group while later groups sort (R18).  d_keys: device buffer of n keys
+ * (scratch + result); workspace as gbs_sort_keys_workspace_size. */
 gbs_status_t gbs_sort_keys_host(uint32_t* h_keys, size_t n, uint32_t* d_keys, void* d_ws,
                                 size_t ws_bytes, gbs_stream_t stream);
+/* The same for key-value pairs (stable by key, as gbs_sort_pairs): h_keys/h_vals pinned
+ * host arrays of n items (in and out), d_keys/d_vals device buffers of n items, workspace
+ * as gbs_sort_pairs_workspace_size. */
+gbs_status_t gbs_sort_pairs_host(uint32_t* h_keys, uint32_t* h_vals, size_t n, uint32_t* d_keys,
+                                 uint32_t* d_vals, void* d_ws, size_t ws_bytes, gbs_stream_t stream);
 
 /* ------------------------------------------------------------ plans, stages */
 

@@ -13,14 +13,15 @@ is present, every call raises.
 from __future__ import annotations
 
 import ctypes as C
+import functools
 import os
 
 __all__ = ["lib", "GbsError", "plan", "workspace_size", "debug_layout", "sort_keys", "sort_pairs",
-           "sort_ex", "sort_keys_host", "Workspace", "get_unique_id", "Comm", "sort_keys_dist",
+           "sort_ex", "sort_keys_host", "sort_pairs_host", "Workspace", "get_unique_id", "Comm", "sort_keys_dist",
            "exchange_plan", "dist_workspace_size"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("GBS_LIB") or os.path.join(_HERE, "libgbs.so")   # GBS_LIB: tuning builds only
+LIB_PATH = os.path.join(_HERE, "libgbs.so")
 MAX_LEVELS = 4
 UNIQUE_ID_BYTES = 128
 
@@ -65,6 +66,7 @@ def lib():
             "gbs_sort_keys": [p, sz, p, sz, p],
             "gbs_sort_pairs": [p, p, sz, p, sz, p],
             "gbs_sort_keys_host": [p, sz, p, p, sz, p],
+            "gbs_sort_pairs_host": [p, p, sz, p, p, p, sz, p],
             "gbs_sort_keys_typed": [p, sz, C.c_int, p, sz, p],
             "gbs_sort_pairs_typed": [p, p, sz, C.c_int, p, sz, p],
             "gbs_plan": [sz, C.c_int, C.POINTER(Config), C.POINTER(PlanT)],
@@ -110,8 +112,8 @@ def _cfg(cfg):
 
 # ----------------------------------------------------------------- plans
 
-def plan(n: int, pairs: bool = False, cfg=None) -> dict:
-    """The static plan for n items (depends on n, kind and cfg only)."""
+@functools.lru_cache(maxsize=256)
+def _plan_cached(n: int, pairs: bool, cfg):
     out = PlanT()
     _check(lib().gbs_plan(n, int(pairs), _cfg(cfg), C.byref(out)))
     k = out.levels
@@ -120,10 +122,13 @@ def plan(n: int, pairs: bool = False, cfg=None) -> dict:
                 kernels_per_sort=out.kernels_per_sort)
 
 
+def plan(n: int, pairs: bool = False, cfg=None) -> dict:
+    """The static plan for n items (depends on n, kind and cfg only)."""
+    return dict(_plan_cached(int(n), bool(pairs), tuple(cfg) if cfg is not None else None))
+
+
 def workspace_size(n: int, pairs: bool = False, cfg=None) -> int:
-    b = C.c_size_t()
-    _check(lib().gbs_workspace_size_ex(n, int(pairs), _cfg(cfg), C.byref(b)))
-    return b.value
+    return _plan_cached(int(n), bool(pairs), tuple(cfg) if cfg is not None else None)["ws_bytes"]
 
 
 def debug_layout(n: int, pairs: bool = False, cfg=None) -> dict:
@@ -152,7 +157,7 @@ def _torch():
     return torch
 
 
-def _dev_ptr(t, name):
+def _dev_ptr(t, name, device=None):
     torch = _torch()
     if not isinstance(t, torch.Tensor) or not t.is_cuda:
         raise GbsError(f"{name} must be a CUDA tensor")
@@ -160,13 +165,53 @@ def _dev_ptr(t, name):
         raise GbsError(f"{name} must be int32/uint32 (bits read as unsigned)")
     if not t.is_contiguous():
         raise GbsError(f"{name} must be contiguous")
+    if device is not None and t.device != device:
+        raise GbsError(f"{name} is on {t.device}, expected {device}")
     return t.data_ptr()
 
 
-def _stream(stream):
-    torch = _torch()
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return C.c_void_p(s.cuda_stream)
+class _On:
+    """Run a library call on `device` (current device = the tensors' device, which is where
+    libgbs launches) with `stream` (default: that device's current stream).  Owns the
+    temporary workspace of the call: allocated with `stream` current, so the caching
+    allocator hands its block to later work only in stream order after the sort; a
+    caller's Workspace used on another stream is marked with record_stream."""
+
+    def __init__(self, device, stream=None):
+        torch = _torch()
+        self.device = device
+        self.stream = stream if stream is not None else torch.cuda.current_stream(device)
+        if self.stream.device != device:
+            raise GbsError(f"stream is on {self.stream.device}, the tensors on {device}")
+        self.keep = []
+
+    def __enter__(self):
+        torch = _torch()
+        self._dg = torch.cuda.device(self.device)
+        self._dg.__enter__()
+        self._sg = torch.cuda.stream(self.stream)
+        self._sg.__enter__()
+        return self
+
+    def __exit__(self, *a):
+        self._sg.__exit__(*a)
+        self._dg.__exit__(*a)
+        self.keep.clear()
+
+    @property
+    def s(self):
+        return C.c_void_p(self.stream.cuda_stream)
+
+    def ws(self, nbytes: int, ws=None):
+        """(pointer, bytes) of a workspace of >= nbytes, alive until the call returns."""
+        torch = _torch()
+        if ws is None:
+            buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
+        else:
+            buf = ws.get(nbytes, self.device)
+            buf.record_stream(self.stream)
+        self.keep.append(buf)
+        return C.c_void_p(buf.data_ptr()), buf.numel()
 
 
 class Workspace:
@@ -176,28 +221,21 @@ class Workspace:
         self.device = device
         self.buf = None
 
-    def get(self, nbytes: int):
+    def get(self, nbytes: int, device=None):
         torch = _torch()
-        if self.buf is None or self.buf.numel() < nbytes:
-            self.buf = torch.empty(max(nbytes, 256), dtype=torch.uint8,
-                                   device=self.device or torch.cuda.current_device())
+        dev = device if device is not None else (self.device if self.device is not None else torch.cuda.current_device())
+        if self.buf is None or self.buf.numel() < nbytes or self.buf.device != torch.device(dev):
+            self.buf = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=dev)
         return self.buf
-
-
-def _ws_for(nbytes, ws, device):
-    if ws is None:
-        ws = Workspace(device)
-    buf = ws.get(nbytes)
-    return C.c_void_p(buf.data_ptr()), buf.numel()
 
 
 def sort_keys(keys, ws: Workspace | None = None, stream=None):
     """Sort a CUDA int32/uint32 tensor in place, ascending as unsigned 32-bit."""
     n = keys.numel()
     kp = _dev_ptr(keys, "keys")
-    need = workspace_size(n)
-    wp, wb = _ws_for(need, ws, keys.device)
-    _check(lib().gbs_sort_keys(C.c_void_p(kp), n, wp, wb, _stream(stream)))
+    with _On(keys.device, stream) as on:
+        wp, wb = on.ws(workspace_size(n), ws)
+        _check(lib().gbs_sort_keys(C.c_void_p(kp), n, wp, wb, on.s))
     return keys
 
 
@@ -206,10 +244,10 @@ def sort_pairs(keys, vals, ws: Workspace | None = None, stream=None):
     n = keys.numel()
     if vals.numel() != n:
         raise GbsError("keys and vals must have the same length")
-    kp, vp = _dev_ptr(keys, "keys"), _dev_ptr(vals, "vals")
-    need = workspace_size(n, pairs=True)
-    wp, wb = _ws_for(need, ws, keys.device)
-    _check(lib().gbs_sort_pairs(C.c_void_p(kp), C.c_void_p(vp), n, wp, wb, _stream(stream)))
+    kp, vp = _dev_ptr(keys, "keys"), _dev_ptr(vals, "vals", keys.device)
+    with _On(keys.device, stream) as on:
+        wp, wb = on.ws(workspace_size(n, pairs=True), ws)
+        _check(lib().gbs_sort_pairs(C.c_void_p(kp), C.c_void_p(vp), n, wp, wb, on.s))
     return keys, vals
 
 
@@ -234,8 +272,9 @@ def sort_keys_typed(keys, key_type=None, ws: Workspace | None = None, stream=Non
     tensor's dtype; floats in IEEE-754 totalOrder, -0 before +0, NaNs at the ends by sign)."""
     kt = _key_type(keys, key_type)
     n = keys.numel()
-    wp, wb = _ws_for(workspace_size(n), ws, keys.device)
-    _check(lib().gbs_sort_keys_typed(C.c_void_p(keys.data_ptr()), n, kt, wp, wb, _stream(stream)))
+    with _On(keys.device, stream) as on:
+        wp, wb = on.ws(workspace_size(n), ws)
+        _check(lib().gbs_sort_keys_typed(C.c_void_p(keys.data_ptr()), n, kt, wp, wb, on.s))
     return keys
 
 
@@ -245,10 +284,10 @@ def sort_pairs_typed(keys, vals, key_type=None, ws: Workspace | None = None, str
     n = keys.numel()
     if vals.numel() != n:
         raise GbsError("keys and vals must have the same length")
-    vp = _dev_ptr(vals, "vals")
-    wp, wb = _ws_for(workspace_size(n, pairs=True), ws, keys.device)
-    _check(lib().gbs_sort_pairs_typed(C.c_void_p(keys.data_ptr()), C.c_void_p(vp), n, kt, wp, wb,
-                                      _stream(stream)))
+    vp = _dev_ptr(vals, "vals", keys.device)
+    with _On(keys.device, stream) as on:
+        wp, wb = on.ws(workspace_size(n, pairs=True), ws)
+        _check(lib().gbs_sort_pairs_typed(C.c_void_p(keys.data_ptr()), C.c_void_p(vp), n, kt, wp, wb, on.s))
     return keys, vals
 
 
@@ -258,33 +297,48 @@ def sort_ex(keys, vals=None, cfg=None, stop_after_step: int = 0, ws=None, stream
     torch = _torch()
     n = keys.numel()
     kp = _dev_ptr(keys, "keys")
-    vp = _dev_ptr(vals, "vals") if vals is not None else None
+    vp = _dev_ptr(vals, "vals", keys.device) if vals is not None else None
     need = workspace_size(n, vals is not None, cfg)
-    if isinstance(ws, torch.Tensor):
-        if ws.numel() < need:
-            raise GbsError("workspace tensor too small")
-        wp, wb = C.c_void_p(ws.data_ptr()), ws.numel()
-    else:
-        wp, wb = _ws_for(need, ws, keys.device)
-    _check(lib().gbs_sort_ex(C.c_void_p(kp), C.c_void_p(vp) if vp else None, n, _cfg(cfg),
-                             stop_after_step, wp, wb, _stream(stream)))
+    with _On(keys.device, stream) as on:
+        if isinstance(ws, torch.Tensor):
+            if ws.numel() < need or ws.device != keys.device:
+                raise GbsError("workspace tensor too small or on another device")
+            wp, wb = C.c_void_p(ws.data_ptr()), ws.numel()
+        else:
+            wp, wb = on.ws(need, ws)
+        _check(lib().gbs_sort_ex(C.c_void_p(kp), C.c_void_p(vp) if vp else None, n, _cfg(cfg),
+                                 stop_after_step, wp, wb, on.s))
     return keys
 
 
 def sort_keys_host(h_keys, d_buf, ws: Workspace | None = None, stream=None):
     """End-to-end: pinned host int32/uint32 tensor -> device -> sort -> host (in place)."""
-    torch = _torch()
     if h_keys.is_cuda or not h_keys.is_pinned():
         raise GbsError("h_keys must be a pinned host tensor")
     n = h_keys.numel()
     dp = _dev_ptr(d_buf, "d_buf")
     if d_buf.numel() < n:
         raise GbsError("d_buf too small")
-    need = workspace_size(n)
-    wp, wb = _ws_for(need, ws, d_buf.device)
-    _check(lib().gbs_sort_keys_host(C.c_void_p(h_keys.data_ptr()), n, C.c_void_p(dp), wp, wb,
-                                    _stream(stream)))
+    with _On(d_buf.device, stream) as on:
+        wp, wb = on.ws(workspace_size(n), ws)
+        _check(lib().gbs_sort_keys_host(C.c_void_p(h_keys.data_ptr()), n, C.c_void_p(dp), wp, wb, on.s))
     return h_keys
+
+
+def sort_pairs_host(h_keys, h_vals, d_keys, d_vals, ws: Workspace | None = None, stream=None):
+    """End-to-end stable pairs sort: pinned host keys/values -> device -> sort -> host (in place)."""
+    for t, nm in ((h_keys, "h_keys"), (h_vals, "h_vals")):
+        if t.is_cuda or not t.is_pinned():
+            raise GbsError(f"{nm} must be a pinned host tensor")
+    n = h_keys.numel()
+    if h_vals.numel() != n or d_keys.numel() < n or d_vals.numel() < n:
+        raise GbsError("size mismatch")
+    dk, dv = _dev_ptr(d_keys, "d_keys"), _dev_ptr(d_vals, "d_vals", d_keys.device)
+    with _On(d_keys.device, stream) as on:
+        wp, wb = on.ws(workspace_size(n, pairs=True), ws)
+        _check(lib().gbs_sort_pairs_host(C.c_void_p(h_keys.data_ptr()), C.c_void_p(h_vals.data_ptr()), n,
+                                         C.c_void_p(dk), C.c_void_p(dv), wp, wb, on.s))
+    return h_keys, h_vals
 
 
 def merge_runs(keys, run_off, ws: Workspace | None = None, stream=None):
@@ -295,8 +349,9 @@ def merge_runs(keys, run_off, ws: Workspace | None = None, stream=None):
     kp = _dev_ptr(keys, "keys")
     need = C.c_size_t()
     _check(lib().gbs_merge_runs_workspace_size(int(off[-1]), p, C.byref(need)))
-    wp, wb = _ws_for(need.value, ws, keys.device)
-    _check(lib().gbs_merge_runs(C.c_void_p(kp), off.ctypes.data_as(C.c_void_p), p, wp, wb, _stream(stream)))
+    with _On(keys.device, stream) as on:
+        wp, wb = on.ws(need.value, ws)
+        _check(lib().gbs_merge_runs(C.c_void_p(kp), off.ctypes.data_as(C.c_void_p), p, wp, wb, on.s))
     return keys
 
 
@@ -356,10 +411,11 @@ def sort_keys_dist(keys, comm: Comm, out=None, ws: Workspace | None = None, stre
     need, cap = dist_workspace_size(n, comm.nranks)
     if out is None or out.numel() < cap:
         out = torch.empty(cap, dtype=keys.dtype, device=keys.device)
-    wp, wb = _ws_for(need, ws, keys.device)
     n_out = C.c_size_t()
-    _check(lib().gbs_sort_keys_dist(comm.handle, C.c_void_p(kp), n, C.c_void_p(out.data_ptr()), out.numel(),
-                                    C.byref(n_out), wp, wb, _stream(stream)))
+    with _On(keys.device, stream) as on:
+        wp, wb = on.ws(need, ws)
+        _check(lib().gbs_sort_keys_dist(comm.handle, C.c_void_p(kp), n, C.c_void_p(out.data_ptr()), out.numel(),
+                                        C.byref(n_out), wp, wb, on.s))
     return out[:n_out.value]
 
 
@@ -376,6 +432,7 @@ def sort_keys_dist_emulated(shards, p: int, stream=None):
     ws = torch.empty(p * need + 256, dtype=torch.uint8, device=shards.device)
     wp = (ws.data_ptr() + 255) // 256 * 256
     n_out = (C.c_size_t * p)()
-    _check(lib().gbs_sort_keys_dist_emulated(p, C.c_void_p(kp), n, C.c_void_p(out.data_ptr()), cap, n_out,
-                                             C.c_void_p(wp), need, _stream(stream)))
+    with _On(shards.device, stream) as on:
+        _check(lib().gbs_sort_keys_dist_emulated(p, C.c_void_p(kp), n, C.c_void_p(out.data_ptr()), cap, n_out,
+                                                 C.c_void_p(wp), need, on.s))
     return [out[r * cap:r * cap + n_out[r]] for r in range(p)]

@@ -31,20 +31,33 @@ def needs_build() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
-    """Compile libgbs.so in-tree (or to `out` with extra -D `defines`, for tuning runs)."""
+    """Compile libgbs.so in-tree (or to `out` with extra -D `defines`, for tuning runs).
+    The translation units compile in parallel, then link."""
     if out is None and not force and not needs_build():
         return LIB
     target = out or LIB
     nccl = nccl_root()
-    cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-           "-Xcompiler", "-fPIC", "-shared", f"-I{nccl}/include",
-           *[os.path.join(CSRC, s) for s in SOURCES],
-           f"-L{nccl}/lib", "-l:libnccl.so.2", "-Xlinker", "-rpath", "-Xlinker", f"{nccl}/lib",
-           *[f"-D{d}" for d in defines],
-           "-o", target + ".tmp"]
+    common = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+              "-Xcompiler", "-fPIC", f"-I{nccl}/include", *[f"-D{d}" for d in defines]]
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-    subprocess.check_call(cmd)
+        common.insert(1, "-Xptxas=-v")
+    tag = f"{os.getpid()}_{abs(hash((target, tuple(defines)))) % 10**8}"
+    objs, procs = [], []
+    for src in SOURCES:
+        obj = os.path.join("/tmp", f"gbs_{tag}_{os.path.splitext(src)[0]}.o")
+        objs.append(obj)
+        procs.append((src, subprocess.Popen(common + ["-c", os.path.join(CSRC, src), "-o", obj])))
+    failed = [src for src, pr in procs if pr.wait() != 0]
+    if failed:
+        raise subprocess.CalledProcessError(1, f"nvcc {failed}")
+    subprocess.check_call([nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", *objs,
+                           f"-L{nccl}/lib", "-l:libnccl.so.2", "-Xlinker", "-rpath", "-Xlinker", f"{nccl}/lib",
+                           "-o", target + ".tmp"])
+    for o in objs:
+        try:
+            os.remove(o)
+        except OSError:
+            pass
     os.replace(target + ".tmp", target)
     return target
 

@@ -96,36 +96,23 @@ __device__ __forceinline__ void reg_sort(T (&x)[M])
 #define GBS_SHFL_LEVELS_WIDE 1   // the same for 8-byte items (u64 composites, pairs): 1 measured +0.9% at C4, 2 slower
 #endif
 
-#ifndef GBS_NARROW_SPLIT
-#define GBS_NARROW_SPLIT 1   // merge chains after the first search a window of H + 1 for their split
-#endif
-
-#ifndef GBS_REV_B
 // Shared-memory merge levels keep the B run of every pair stored descending (a bitonic
-// pair): a merge pointer that runs past the end of its run then walks down the other
-// run from its far end, so no end-of-run checks are needed (see merge_thread)
-#define GBS_REV_B 1
-#endif
+// pair): a merge pointer that runs past the end of its run then walks down the other run
+// from its far end, so no end-of-run checks are needed (see merge_thread).
 
-#ifndef GBS_PAD_SHIFT
-#define GBS_PAD_SHIFT 0   // 0 = one pad slot per ITEMS
-#endif
-
-template <typename T, int BLOCK, int ITEMS, int CHAINS_ = 0, int PAD_ = GBS_PAD_SHIFT>
+template <typename T, int BLOCK, int ITEMS, int CHAINS_ = 0>
 struct CtaSort {
     static constexpr int TILE = BLOCK * ITEMS;
     // A tile that is not a power of two (BLOCK not a power of two, e.g. 544 x 32) has a
-    // short last run at some levels; with B runs stored descending (GBS_REV_B) the merge
-    // handles it by clipping the pair's run lengths (la, lb), nothing else changes.
+    // short last run at some levels; with B runs stored descending the merge handles it by
+    // clipping the pair's run lengths (la, lb), nothing else changes.
     static constexpr bool POW2_TILE = (TILE & (TILE - 1)) == 0;
-    static_assert(POW2_TILE || GBS_REV_B, "non-power-of-two tiles need GBS_REV_B");
     static constexpr int LOG_ITEMS = Ctz<ITEMS>::value;   // log2(ITEMS) for a power of two
     static constexpr int WARP_SPAN = 32 * ITEMS;                  // items owned by one warp
     // Shared-memory layout: one pad slot every 2^PAD items.  PAD = ctz(ITEMS) (log2 for a
     // power of two) makes a thread's stride ITEMS + ITEMS/2^PAD odd, so the blocked
-    // stores are conflict-free; a finer pad spreads the merge reads, whose lanes sit
-    // ~ITEMS/2 elements apart in each run.
-    static constexpr int PAD = PAD_ > 0 ? PAD_ : LOG_ITEMS;
+    // stores are conflict-free.
+    static constexpr int PAD = LOG_ITEMS;
     static constexpr int SMEM_ELEMS = TILE + (TILE >> PAD) + 2;
     // independent merge chains per thread (ILP); overridable by the instantiation
     static constexpr int CHAINS = CHAINS_ > 0 ? CHAINS_ : ((ITEMS * sizeof(T) <= 256) ? 2 : 1);
@@ -135,7 +122,6 @@ struct CtaSort {
         ((ITEMS & (ITEMS - 1)) == 0 && ITEMS >= 2) ? (sizeof(T) == 4 ? GBS_SHFL_LEVELS : GBS_SHFL_LEVELS_WIDE) : 0;
 
     static __device__ __forceinline__ int phys(int p) { return p + (p >> PAD); }
-    static __device__ __forceinline__ int phys_fma(int p) { return p + (p >> PAD); }
 
     // Position of register slot k of the calling thread in the load order: each warp
     // owns a contiguous span of 32*ITEMS positions, read 32 consecutive at a time
@@ -147,21 +133,15 @@ struct CtaSort {
     }
 
     // Merge-path split of output diagonal `diag` of the pair (A = [a0, a0+w),
-    // B = [a0+w, a0+2w)): number of outputs taken from A (ties: A first -> stable).
-    static __device__ __forceinline__ int split(const T* sm, int a0, int w, int diag)
-    {
-        return split_in(sm, a0, w, diag, max(0, diag - w), min(diag, w));
-    }
-    // the same, knowing the split lies in [lo, hi]
+    // B = [a0+w, a0+2w), B stored descending), knowing the split lies in [lo, hi]: the
+    // number of outputs taken from A (ties: A first -> stable).  B[diag-1-mid] sits at
+    // a0 + 2w - 1 - (diag - 1 - mid) = bt + mid.
     static __device__ __forceinline__ int split_in(const T* sm, int a0, int w, int diag, int lo, int hi)
     {
-        // B[diag-1-mid] sits at b0 + diag - 1 - mid, or (B descending, GBS_REV_B) at
-        // a0 + 2w - 1 - (diag - 1 - mid) = bt + mid
-        const int b0 = a0 + w, bt = a0 + 2 * w - diag;
+        const int bt = a0 + 2 * w - diag;
         while (lo < hi) {
             const int mid = (lo + hi) >> 1;
-            const int bpos = GBS_REV_B ? bt + mid : b0 + diag - 1 - mid;
-            if (sm[phys(a0 + mid)] <= sm[phys(bpos)]) lo = mid + 1;
+            if (sm[phys(a0 + mid)] <= sm[phys(bt + mid)]) lo = mid + 1;
             else hi = mid;
         }
         return lo;
@@ -181,13 +161,13 @@ struct CtaSort {
 
     // Store the thread's ITEMS outputs [start, start+ITEMS), which belong to runs of
     // length w: ascending, or mirrored inside the run when the run is the B of the next
-    // level's pair (odd run index, GBS_REV_B).  `rev` is warp-uniform once w >= 32 ITEMS.
+    // level's pair (odd run index).  The branch is warp-uniform once w >= 32 ITEMS.
     // lg = log2(w / ITEMS): the run of thread t is t >> lg (start = t ITEMS).
     template <int M>
     static __device__ __forceinline__ void store_run(const T (&x)[M], T* sm, int start, int w, int lg)
     {
         const int q = (int)threadIdx.x >> lg;                 // run index
-        if (GBS_REV_B && (q & 1)) {
+        if (q & 1) {
             const int r0 = (q << lg) * ITEMS;                 // run start
             const int lr = POW2_TILE ? w : min(w, TILE - r0); // run length (the tile's last run may be short)
             const int e = 2 * r0 + lr - ITEMS - start;        // mirrored block start
@@ -209,19 +189,14 @@ struct CtaSort {
     // interleaved for ILP (each step of a chain waits on one shared-memory load).
     // Ties take A first, so the merge is stable.
     //
-    // GBS_REV_B: B is stored descending (B[j] at base + 2w - 1 - j).  Per chain only the
-    // A position ai is kept; the B head sits at ai + E - k after k outputs.  A pointer
-    // that passes the end of its run reads the other run from its far end (its largest
-    // remaining item), so every output is still the smallest remaining item and no
-    // end-of-run check is needed: the two pointers consume the remaining items from both
-    // ends and never cross within the thread's outputs.  The only items that can then be
-    // taken "from the wrong side" are equal to the true output: keys (values only) are
-    // unaffected, and 8-byte items (u64 composites, pairs as key<<32|position) are
-    // distinct.
-    //
-    // Otherwise (B ascending): B's index is (2 base + w + diag) - A index, and an
-    // exhausted run reads as TMAX ("sticky sentinel"), with a warp-uniform fast path when
-    // no lane can exhaust a run inside its outputs.
+    // B is stored descending (B[j] at base + 2w - 1 - j).  Per chain only the A position
+    // ai is kept; the B head sits at ai + E - k after k outputs.  A pointer that passes
+    // the end of its run reads the other run from its far end (its largest remaining
+    // item), so every output is still the smallest remaining item and no end-of-run check
+    // is needed: the two pointers consume the remaining items from both ends and never
+    // cross within the thread's outputs.  The only items that can then be taken "from the
+    // wrong side" are equal to the true output: keys (values only) are unaffected, and
+    // 8-byte items (u64 composites, pairs as key<<32|position) are distinct.
     template <int M>
     static __device__ __forceinline__ void merge_thread(T (&x)[M], const T* sm, int start, int w)
     {
@@ -230,7 +205,6 @@ struct CtaSort {
         // w = ITEMS * 2^k; ITEMS itself need not be a power of two (the pair index is
         // taken on the thread index start / ITEMS)
         const int base = ((start / ITEMS) & ~(2 * (w / ITEMS) - 1)) * ITEMS;
-        const int aEnd = base + w, bEnd = base + 2 * w;
         // run lengths of the pair (a short last run only in a non-power-of-two tile: then
         // B is empty or A is full); B's first item sits at `top` (B descending)
         const int la = POW2_TILE ? w : min(w, TILE - base);
@@ -245,60 +219,15 @@ struct CtaSort {
         for (int c = 0; c < CHAINS; ++c) {
             const int diag = start - base + c * H;
             if (POW2_TILE)
-                sp = c == 0 || !GBS_NARROW_SPLIT ? split(sm, base, w, diag)
-                                                 : split_in(sm, base, w, diag, max(sp, diag - w), min(sp + H, min(diag, w)));
+                sp = c == 0 ? split_in(sm, base, w, diag, max(0, diag - w), min(diag, w))
+                            : split_in(sm, base, w, diag, max(sp, diag - w), min(sp + H, min(diag, w)));
             else
                 sp = split_top(sm, base, top, diag, c == 0 ? max(0, diag - lb) : max(sp, diag - lb),
                                c == 0 ? min(diag, la) : min(sp + H, min(diag, la)));
             ai[c] = base + sp;
-            if (GBS_REV_B) {
-                cb[c] = top - base - diag;                // E: B head = ai + E - k
-                a[c] = sm[phys(ai[c])];
-                b[c] = sm[phys(ai[c] + cb[c])];
-            } else {
-                cb[c] = 2 * base + w + diag;              // bi = cb - ai
-                const int bi = cb[c] - ai[c];
-                a[c] = ai[c] < aEnd ? sm[phys(ai[c])] : TMAX;
-                b[c] = bi < bEnd ? sm[phys(bi)] : TMAX;
-            }
-        }
-        if (GBS_REV_B) {
-#pragma unroll
-            for (int k = 0; k < H; ++k) {
-#pragma unroll
-                for (int c = 0; c < CHAINS; ++c) {
-                    const bool t = a[c] <= b[c];
-                    x[c * H + k] = t ? a[c] : b[c];
-                    const int bnext = ai[c] + cb[c] - (k + 1);
-                    ai[c] += t ? 1 : 0;
-                    const int nidx = t ? ai[c] : bnext;
-                    const T v = sm[phys_fma(nidx)];
-                    a[c] = t ? v : a[c];
-                    b[c] = t ? b[c] : v;
-                }
-            }
-            return;
-        }
-        // Fast path (warp-uniform): no lane can exhaust a run inside its H outputs, so
-        // the end-of-run checks (3 ALU-pipe ops per step) are dropped.
-        bool fast = true;
-#pragma unroll
-        for (int c = 0; c < CHAINS; ++c) fast = fast && ai[c] + H <= aEnd && cb[c] - ai[c] + H <= bEnd;
-        if (__all_sync(__activemask(), fast)) {
-#pragma unroll
-            for (int k = 0; k < H; ++k) {
-#pragma unroll
-                for (int c = 0; c < CHAINS; ++c) {
-                    const bool t = a[c] <= b[c];
-                    x[c * H + k] = t ? a[c] : b[c];
-                    ai[c] += t ? 1 : 0;
-                    const int nidx = t ? ai[c] : cb[c] + k + 1 - ai[c];
-                    const T v = sm[phys_fma(nidx)];
-                    a[c] = t ? v : a[c];
-                    b[c] = t ? b[c] : v;
-                }
-            }
-            return;
+            cb[c] = top - base - diag;                    // E: B head = ai + E - k
+            a[c] = sm[phys(ai[c])];
+            b[c] = sm[phys(ai[c] + cb[c])];
         }
 #pragma unroll
         for (int k = 0; k < H; ++k) {
@@ -306,12 +235,10 @@ struct CtaSort {
             for (int c = 0; c < CHAINS; ++c) {
                 const bool t = a[c] <= b[c];
                 x[c * H + k] = t ? a[c] : b[c];
+                const int bnext = ai[c] + cb[c] - (k + 1);
                 ai[c] += t ? 1 : 0;
-                const int bi = cb[c] + k + 1 - ai[c];
-                const int nidx = t ? ai[c] : bi;
-                const bool ok = nidx < (t ? aEnd : bEnd);
-                T v = sm[phys_fma(nidx)];
-                v = ok ? v : TMAX;
+                const int nidx = t ? ai[c] : bnext;
+                const T v = sm[phys(nidx)];
                 a[c] = t ? v : a[c];
                 b[c] = t ? b[c] : v;
             }
@@ -385,7 +312,7 @@ struct CtaSort {
                 x[k] = t ? a : b;
                 ai += t ? 1 : 0;
                 const int nidx = t ? ai : cb + k - ai;
-                const T v = sm[phys_fma(nidx)];
+                const T v = sm[phys(nidx)];
                 a = t ? v : a;
                 b = t ? b : v;
             }
@@ -420,12 +347,12 @@ struct CtaSort {
             const int p = t + k * BLOCK;
             x[k] = p < valid ? src[p] : TMAX;
         }
-        // odd runs of R stored mirrored (GBS_REV_B): the B of each first-level pair
+        // odd runs of R stored mirrored: the B of each first-level pair
 #pragma unroll
         for (int k = 0; k < ITEMS; ++k) {
             const int p = t + k * BLOCK;
             const int r0 = p & ~(R - 1);
-            sm[phys(GBS_REV_B && (p & R) && R < TILE ? 2 * r0 + R - 1 - p : p)] = x[k];
+            sm[phys((p & R) && R < TILE ? 2 * r0 + R - 1 - p : p)] = x[k];
         }
         __syncthreads();
         const int start = t * ITEMS;
@@ -437,18 +364,13 @@ struct CtaSort {
             const bool active = intra ? (wspan0 < valid) : (start < valid);
             if (active) merge_thread(x, sm, start, w);
             if (intra) __syncwarp(); else __syncthreads();
-            if (GBS_REV_B) {
-                // every position is rewritten (the layout of the sentinel tail changes
-                // with the run parity); idle threads' outputs are all sentinels
-                if (!active) {
+            // every position is rewritten (the layout of the sentinel tail changes with
+            // the run parity); idle threads' outputs are all sentinels
+            if (!active) {
 #pragma unroll
-                    for (int k = 0; k < ITEMS; ++k) x[k] = TMAX;
-                }
-                store_run(x, sm, start, 2 * w, lg + 1);
-            } else if (active) {
-#pragma unroll
-                for (int k = 0; k < ITEMS; ++k) sm[phys(start + k)] = x[k];
+                for (int k = 0; k < ITEMS; ++k) x[k] = TMAX;
             }
+            store_run(x, sm, start, 2 * w, lg + 1);
             // the NEXT level's readers decide the barrier: a cross-warp level reads
             // other warps' stores
             if (4 * w <= WARP_SPAN) __syncwarp(); else __syncthreads();

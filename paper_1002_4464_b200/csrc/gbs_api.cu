@@ -96,10 +96,6 @@ constexpr uint64_t SMALL_U64_TOTAL = 1u << 18;   // u64 levels up to this many s
 #ifndef GBS_SMALL_N_KEYS
 #define GBS_SMALL_N_KEYS (1u << 17)   // keys problems up to this size use 2K sublists and buckets (0 = off)
 #endif
-#ifndef GBS_U64_MED_TOTAL
-#define GBS_U64_MED_TOTAL 0                       // ... and up to this many 8K tiles (0 = off; measured slower at C2/C3)
-#endif
-constexpr uint32_t MED_TILE_U64 = 8192;
 constexpr uint32_t D_MIN = 8;              // single level needs d >= 8
 constexpr uint32_t D_NEST = 32;            // d of a level with a nested Step 9
 constexpr uint32_t MAX_S = 4096;           // shared-memory limit of Steps 6 and 8
@@ -274,15 +270,9 @@ static int build_node(Plan& P, int kind, uint32_t B, uint64_t N, uint32_t pad_ba
             for (uint32_t c = 2; c <= SMALL_TILE / D_MIN && !s; c *= 2)
                 if (hi_bound(N, SMALL_TILE, c) <= SMALL_TILE) s = c;
         }
+        // (8K tiles for mid-size u64 levels measured slower at C2 and C3)
         if (s) {
             L = SMALL_TILE;
-        } else if (kind == KIND_U64 && (uint64_t)B * N <= GBS_U64_MED_TOTAL) {
-            // mid-size u64 level: half tiles (twice the CTAs) when one level with d >= D_MIN fits
-            for (uint32_t c = 2; c <= MED_TILE_U64 / D_MIN; c *= 2)
-                if (hi_bound(N, MED_TILE_U64, c) <= MED_TILE_U64) { s = c; break; }
-            if (s) L = MED_TILE_U64;
-        }
-        if (s) {
         } else {
             L = tile;
             for (uint32_t c = 2; c <= L / D_MIN; c *= 2)
@@ -387,15 +377,6 @@ static gbs_status_t make_plan(size_t n, int kind, const gbs_config_t* cfg, Plan&
 // ----------------------------------------------------------------- launches
 static uint32_t num_sms();
 constexpr int S4_MERGE_BLOCK = 256, S4_MERGE_ITEMS = 16;
-#ifndef GBS_SPLIT_STEP9
-#define GBS_SPLIT_STEP9 1
-#endif
-#ifndef GBS_FUSE_89
-#define GBS_FUSE_89 1     // fused Step 8+9 for CTA-bucket levels
-#endif
-#ifndef GBS_FUSE_MIN_D
-#define GBS_FUSE_MIN_D 32 // ... whose average run d = L/s is at least this many items
-#endif
 #ifndef GBS_IDX_TMA
 #define GBS_IDX_TMA 1
 #endif
@@ -429,17 +410,43 @@ static void set_smem(K kernel, size_t bytes)
     if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
+// One-time setup per device and kernel: the dynamic shared-memory opt-in is a function
+// attribute of the current device, so a process that sorts on several GPUs configures
+// each of them (and caches the occupancy the setup returns per device).
+constexpr int MAX_DEVICES = 64;
+static int cur_device()
+{
+    int d = 0;
+    cudaGetDevice(&d);
+    return (d >= 0 ? d : 0) % MAX_DEVICES;
+}
+struct DevOnce {
+    std::once_flag f[MAX_DEVICES];
+    int val[MAX_DEVICES] = {};
+    template <typename F>
+    int run(F&& fn)
+    {
+        const int d = cur_device();
+        std::call_once(f[d], [&] { val[d] = fn(); });
+        return val[d];
+    }
+};
+template <typename K>
+static int occupancy(K kernel, int block, size_t smem)
+{
+    int occ = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, block, smem) != cudaSuccess || occ < 1) occ = 1;
+    return occ;
+}
+
 template <int KIND, int BLOCK, int ITEMS>
 static void launch_local_t(const LevelDev& lv0, cudaStream_t st)
 {
     const size_t sm = Seg<KIND, BLOCK, ITEMS>::smem_bytes();
-    static std::once_flag f;
-    static int occ = 1;
-    std::call_once(f, [&] {
+    static DevOnce once;
+    const int occ = once.run([&] {
         set_smem(k_local_sort<KIND, BLOCK, ITEMS>, sm);
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_local_sort<KIND, BLOCK, ITEMS>, BLOCK, sm) !=
-                cudaSuccess || occ < 1)
-            occ = 1;
+        return occupancy(k_local_sort<KIND, BLOCK, ITEMS>, BLOCK, sm);
     });
     // persistent: one CTA per resident slot, each walks tiles blockIdx.x + k*gridDim.x
     const unsigned grid = std::min<unsigned>(lv0.B * lv0.m, num_sms() * (unsigned)occ);
@@ -453,15 +460,11 @@ static void launch_seg_t(const LevelDev& lv, unsigned count, cudaStream_t st)
     const size_t sm = MODE == MODE_GATHER
                           ? gather_smem_offset<KIND, BLOCK, ITEMS>() + ((size_t)gather_max_m(KIND) + 1) * 8
                           : Seg<KIND, BLOCK, ITEMS>::smem_bytes();
-    static std::once_flag f;
-    static int occ = 1;
-    std::call_once(f, [&] {
+    static DevOnce once;
+    once.run([&] {
         set_smem(k_segment_sort<KIND, BLOCK, ITEMS, MODE>, sm);
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_segment_sort<KIND, BLOCK, ITEMS, MODE>, BLOCK,
-                                                          sm) != cudaSuccess || occ < 1)
-            occ = 1;
+        return 1;
     });
-    (void)occ;
     // one CTA per segment (for a size tier: per list slot, the unused tail exits at once)
     launch_k(k_segment_sort<KIND, BLOCK, ITEMS, MODE>, count, BLOCK, sm, st, lv);
 }
@@ -474,13 +477,10 @@ template <int KIND, int BLOCK, int ITEMS>
 static void launch_rare_t(const LevelDev& lv, unsigned count, cudaStream_t st)
 {
     const size_t sm = Seg<KIND, BLOCK, ITEMS>::smem_bytes();
-    static std::once_flag f;
-    static int occ = 1;
-    std::call_once(f, [&] {
+    static DevOnce once;
+    const int occ = once.run([&] {
         set_smem(k_segment_sort_rare<KIND, BLOCK, ITEMS>, sm);
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_segment_sort_rare<KIND, BLOCK, ITEMS>, BLOCK, sm) !=
-                cudaSuccess || occ < 1)
-            occ = 1;
+        return occupancy(k_segment_sort_rare<KIND, BLOCK, ITEMS>, BLOCK, sm);
     });
     launch_k(k_segment_sort_rare<KIND, BLOCK, ITEMS>, std::min<unsigned>(count, num_sms() * (unsigned)occ), BLOCK, sm,
              st, lv);
@@ -491,8 +491,11 @@ static void launch_local_pair(const LevelDev& lv, cudaStream_t st)
 {
     constexpr int BLOCK = GBS_KEYS_BLOCK, ITEMS = GBS_KEYS_ITEMS;
     const size_t sm = Seg<KIND_KEYS, BLOCK, ITEMS>::smem_bytes();
-    static std::once_flag f;
-    std::call_once(f, [&] { set_smem(k_local_sort_pair<BLOCK, ITEMS>, sm); });
+    static DevOnce once;
+    once.run([&] {
+        set_smem(k_local_sort_pair<BLOCK, ITEMS>, sm);
+        return 1;
+    });
     const unsigned pairs = std::min<unsigned>(lv.B * lv.m, num_sms() / 2);
     launch_k(k_local_sort_pair<BLOCK, ITEMS>, 2 * pairs, BLOCK, sm, st, lv);
 }
@@ -502,10 +505,7 @@ static void launch_local(const LevelDev& lv, bool small, cudaStream_t st)
 {
     if (small) launch_local_t<KIND, GBS_SMALL>(lv, st);
     else if constexpr (KIND == KIND_KEYS) launch_local_t<KIND, GBS_BIG_KEYS>(lv, st);
-    else if constexpr (KIND == KIND_U64 && GBS_U64_MED_TOTAL > 0) {
-        if (lv.L == MED_TILE_U64) launch_local_t<KIND, 512, 16>(lv, st);
-        else launch_local_t<KIND, GBS_BIG_WIDE>(lv, st);
-    } else launch_local_t<KIND, GBS_BIG_WIDE>(lv, st);
+    else launch_local_t<KIND, GBS_BIG_WIDE>(lv, st);
 }
 
 template <int KIND, int MODE>
@@ -525,15 +525,11 @@ static void launch_index(const LevelDev& lv, cudaStream_t st)
                      (lv.pr.stride * kb) % 16 == 0 && ((size_t)lv.L * kb) % 16 == 0 && lv.s <= 8 * IDX_BLOCK;
     if (tma) {
         const size_t sm = 2 * (size_t)IDX_CHUNK_BYTES + (size_t)lv.s * 12;
-        static std::once_flag f2;
-        static int occ = 1;
-        std::call_once(f2, [&] {
+        static DevOnce once;
+        const int occ = once.run([&] {
             set_smem(k_sample_index_tma<KIND, IDX_BLOCK, 8>, 220 * 1024);
             // occupancy at the largest table this kernel sees (s <= 4096)
-            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_sample_index_tma<KIND, IDX_BLOCK, 8>, IDX_BLOCK,
-                                                              2 * (size_t)IDX_CHUNK_BYTES + 4096 * 12) != cudaSuccess ||
-                occ < 1)
-                occ = 1;
+            return occupancy(k_sample_index_tma<KIND, IDX_BLOCK, 8>, IDX_BLOCK, 2 * (size_t)IDX_CHUNK_BYTES + 4096 * 12);
         });
         const unsigned grid = std::min<unsigned>(lv.B * lv.m, num_sms() * (unsigned)occ);
         launch_k(k_sample_index_tma<KIND, IDX_BLOCK, 8>, grid, IDX_BLOCK, sm, st, lv);
@@ -541,8 +537,11 @@ static void launch_index(const LevelDev& lv, cudaStream_t st)
     }
     const size_t chunk = std::min<size_t>((size_t)lv.L * key_bytes(KIND), IDX_CHUNK_BYTES);
     const size_t sm = (size_t)lv.s * 8 + (size_t)(lv.s + (lv.s & 1)) * 4 + chunk;
-    static std::once_flag f;
-    std::call_once(f, [&] { set_smem(k_sample_index<KIND, IDX_BLOCK>, 227 * 1024); });
+    static DevOnce once;
+    once.run([&] {
+        set_smem(k_sample_index<KIND, IDX_BLOCK>, 227 * 1024);
+        return 1;
+    });
     launch_k(k_sample_index<KIND, IDX_BLOCK>, lv.B * lv.m, IDX_BLOCK, sm, st, lv);
 }
 
@@ -582,8 +581,11 @@ static void launch_relocate(const LevelDev& lv, cudaStream_t st)
     constexpr int MAXPER = (int)(tile_of_c(KIND) / IDX_BLOCK);
     const size_t per = std::max<size_t>(1, lv.L / IDX_BLOCK);
     const size_t sm = (size_t)2 * lv.s * 4 + (lv.L + 2 * (lv.L / per) + 4) * 2;
-    static std::once_flag f;
-    std::call_once(f, [&] { set_smem(k_relocate<KIND, IDX_BLOCK, MAXPER>, 220 * 1024); });
+    static DevOnce once;
+    once.run([&] {
+        set_smem(k_relocate<KIND, IDX_BLOCK, MAXPER>, 220 * 1024);
+        return 1;
+    });
     LevelDev lr = lv;   // the per-sublist form defers to the grouped one only if that was launched
     if (!(GROUP > 0 && lv.pex)) lr.maxrun = nullptr;
     launch_k(k_relocate<KIND, IDX_BLOCK, MAXPER>, lv.B * lv.m, IDX_BLOCK, sm, st, lr);
@@ -591,13 +593,13 @@ static void launch_relocate(const LevelDev& lv, cudaStream_t st)
 
 static uint32_t num_sms()
 {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
+    static DevOnce once;
+    return (uint32_t)once.run([] {
+        int n = 0, dev = 0;
         cudaGetDevice(&dev);
         if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
-    }
-    return (uint32_t)n;
+        return n;
+    });
 }
 
 // A second stream per device for work that runs beside the call's stream inside one
@@ -616,11 +618,23 @@ static cudaStream_t side_stream(int k = 0)   // k: 0 = Step 9 tiers, 1 = H2D, 2 
     return ss[dev][k];
 }
 
+// Events for fork/join inside one call, created once per thread and device and reused:
+// cudaStreamWaitEvent waits for the record that precedes it, so a later re-record of the
+// same event (next chunk, next call) does not affect an earlier wait.
+static cudaEvent_t scratch_event(int k)
+{
+    static thread_local cudaEvent_t ev[MAX_DEVICES][8] = {};
+    const int d = cur_device();
+    if (!ev[d][k] && cudaEventCreateWithFlags(&ev[d][k], cudaEventDisableTiming) != cudaSuccess) ev[d][k] = nullptr;
+    return ev[d][k];
+}
+
 // Host-buffer calls (gbs_sort_keys_host): the H2D copy is split into chunks of sublists
 // and Step 2 sorts each chunk as it lands; Step 9 runs in groups of buckets and each
 // group's final output range is copied back while the next groups sort.
 struct HostPipe {
     uint32_t* h;              // pinned host keys (in and out)
+    uint32_t* hv;             // pinned host values (pairs) or nullptr
     size_t n;
     cudaStream_t cin, cout;   // copy streams
 };
@@ -664,8 +678,11 @@ static gbs_status_t launch_s4_tree(const Node& nd, const LevelDev& lv, char* ws,
     u64* cur = (nd.s4_levels % 2 == 0) ? T : S;
     u64* oth = cur == T ? S : T;
     const size_t sm = sizeof(u64) * CtaSort<unsigned long long, TB, TI>::SMEM_ELEMS;
-    static std::once_flag f;
-    std::call_once(f, [&] { set_smem(k_s4_tile<TB, TI>, sm); });
+    static DevOnce once;
+    once.run([&] {
+        set_smem(k_s4_tile<TB, TI>, sm);
+        return 1;
+    });
     launch_k(k_s4_tile<TB, TI>, (N + TILE - 1) / TILE, TB, sm, st, (const u64*)S, cur, N, nd.s);
     GBS_LAUNCHED();
     constexpr uint32_t TO = S4_MERGE_BLOCK * S4_MERGE_ITEMS;
@@ -716,11 +733,8 @@ static gbs_status_t launch_step9(const LevelDev& lv, const Node& nd, char* ws, c
             // sort) on the side stream, so they are not a serial tail after tier 0.
             // (tier 1 on one side stream; tiers 2 and 3 -- usually empty -- on another)
             cudaStream_t ss = side_stream(), ss2 = side_stream(3);
-            cudaEvent_t fork = nullptr, join = nullptr, join2 = nullptr;
-            if (ss && ss2) {
-                GBS_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
-                GBS_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
-                GBS_CUDA(cudaEventCreateWithFlags(&join2, cudaEventDisableTiming));
+            cudaEvent_t fork = scratch_event(0), join = scratch_event(1), join2 = scratch_event(2);
+            if (ss && ss2 && fork && join && join2) {
                 GBS_CUDA(cudaEventRecord(fork, st));
                 GBS_CUDA(cudaStreamWaitEvent(ss, fork, 0));
                 GBS_CUDA(cudaStreamWaitEvent(ss2, fork, 0));
@@ -765,9 +779,6 @@ static gbs_status_t launch_step9(const LevelDev& lv, const Node& nd, char* ws, c
                 GBS_CUDA(cudaEventRecord(join2, ss2));
                 GBS_CUDA(cudaStreamWaitEvent(st, join, 0));
                 GBS_CUDA(cudaStreamWaitEvent(st, join2, 0));
-                cudaEventDestroy(fork);
-                cudaEventDestroy(join);
-                cudaEventDestroy(join2);
             }
         } else {
             launch_seg<KIND, MODE>(lv, nd.bucket_small, nd.B * nd.s, st);
@@ -838,20 +849,19 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
     // Steps 2-3: local sort + local samples (one CTA per sublist)
     if (hp) {
         // chunk c of sublists is copied in on hp->cin, then sorted on st
-        cudaEvent_t ev;
-        GBS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        cudaEvent_t ev = scratch_event(3);
+        if (!ev) return fail(GBS_ERROR_CUDA, "cannot create an event");
         GBS_CUDA(cudaEventRecord(ev, st));                  // d_keys free (earlier work on st)
         GBS_CUDA(cudaStreamWaitEvent(hp->cin, ev, 0));
-        cudaEventDestroy(ev);
         uint32_t* dk = reinterpret_cast<uint32_t*>(lv.in);
         for (uint32_t t0 = 0; t0 < nd.m; t0 += HP_CHUNK_TILES) {
             const uint32_t t1 = std::min(nd.m, t0 + HP_CHUNK_TILES);
             const size_t e0 = (size_t)t0 * nd.L, e1 = std::min(hp->n, (size_t)t1 * nd.L);
             GBS_CUDA(cudaMemcpyAsync(dk + e0, hp->h + e0, (e1 - e0) * 4, cudaMemcpyHostToDevice, hp->cin));
-            GBS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            if (hp->hv)
+                GBS_CUDA(cudaMemcpyAsync(lv.in_v + e0, hp->hv + e0, (e1 - e0) * 4, cudaMemcpyHostToDevice, hp->cin));
             GBS_CUDA(cudaEventRecord(ev, hp->cin));
             GBS_CUDA(cudaStreamWaitEvent(st, ev, 0));
-            cudaEventDestroy(ev);
             LevelDev lc = lv;
             lc.tile_lo = t0;
             lc.tile_hi = t1;
@@ -932,7 +942,7 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
     pm.mark();
 
     // Step 9: bucket sort reloc -> out (one CTA per bucket) or a nested level
-    if (hp) {
+    if (hp && nd.step9 < 0) {
         // groups of buckets; after buckets [0, j1) are sorted, the output prefix
         // [0, j1 m d - V) is final: exactly j1 m samples are <= g_{j1-1}, and a sublist
         // with c samples <= g has >= c d items <= g, so >= j1 m d items (V of them
@@ -940,7 +950,8 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
         const uint64_t V = (uint64_t)nd.m * nd.L - hp->n;
         const uint32_t G = std::max(1u, nd.s / HP_GROUPS);
         uint64_t done = 0;
-        cudaEvent_t ev;
+        cudaEvent_t ev = scratch_event(4);
+        if (!ev) return fail(GBS_ERROR_CUDA, "cannot create an event");
         for (uint32_t j0 = 0; j0 < nd.s; j0 += G) {
             const uint32_t j1 = std::min(nd.s, j0 + G);
             LevelDev lg = lv;
@@ -951,19 +962,18 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
             const uint64_t lo_cnt = (uint64_t)j1 * nd.m * nd.d;
             const uint64_t upto = j1 == nd.s ? hp->n : std::min<uint64_t>(hp->n, lo_cnt > V ? lo_cnt - V : 0);
             if (upto > done) {
-                GBS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
                 GBS_CUDA(cudaEventRecord(ev, st));
                 GBS_CUDA(cudaStreamWaitEvent(hp->cout, ev, 0));
-                cudaEventDestroy(ev);
                 GBS_CUDA(cudaMemcpyAsync(hp->h + done, reinterpret_cast<uint32_t*>(lv.out) + done, (upto - done) * 4,
                                          cudaMemcpyDeviceToHost, hp->cout));
+                if (hp->hv)
+                    GBS_CUDA(cudaMemcpyAsync(hp->hv + done, lv.out_v + done, (upto - done) * 4, cudaMemcpyDeviceToHost,
+                                             hp->cout));
                 done = upto;
             }
         }
-        GBS_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
         GBS_CUDA(cudaEventRecord(ev, hp->cout));
         GBS_CUDA(cudaStreamWaitEvent(st, ev, 0));          // the call completes on st
-        cudaEventDestroy(ev);
     } else if (nd.step9 < 0) {
         gbs_status_t r9;
         if constexpr (KIND == KIND_KEYS)
@@ -988,14 +998,15 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
 
 static gbs_status_t check_device()
 {
-    static int ok = -1;
-    if (ok < 0) {
-        int dev = 0, major = 0;
-        if (cudaGetDevice(&dev) != cudaSuccess) return fail(GBS_ERROR_CUDA, "no CUDA device");
-        if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess)
-            return fail(GBS_ERROR_CUDA, "cannot query device");
-        ok = major == 10 ? 1 : 0;
-    }
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return fail(GBS_ERROR_CUDA, "no CUDA device");
+    static DevOnce once;   // 1 = sm_100, 0 = other, -1 = query failed
+    const int ok = once.run([dev] {
+        int major = 0;
+        if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess) return -1;
+        return major == 10 ? 1 : 0;
+    });
+    if (ok < 0) return fail(GBS_ERROR_CUDA, "cannot query device");
     return ok ? GBS_SUCCESS : fail(GBS_ERROR_UNSUPPORTED, "device is not sm_100 (Blackwell B200)");
 }
 
@@ -1219,40 +1230,70 @@ gbs_status_t gbs_sort_ex(uint32_t* d_keys, uint32_t* d_vals, size_t n, const gbs
     return run_sort(d_keys, d_vals, n, cfg, stop_after_step, d_ws, ws_bytes, (cudaStream_t)stream);
 }
 
-gbs_status_t gbs_sort_keys_host(uint32_t* h_keys, size_t n, uint32_t* d_keys, void* d_ws, size_t ws_bytes,
-                                gbs_stream_t stream)
+// End to end from pinned host buffers (keys, or keys + values).  Above HP_CHUNK_TILES
+// sublists the H2D copy is chunked so Step 2 sorts each chunk as it lands; with CTA
+// buckets (one level) the D2H copy of each bucket group's final output prefix (R18)
+// overlaps the remaining Step 9 groups; with a nested Step 9 the D2H copy follows it.
+static gbs_status_t run_sort_host(uint32_t* h_keys, uint32_t* h_vals, size_t n, uint32_t* d_keys, uint32_t* d_vals,
+                                  void* d_ws, size_t ws_bytes, cudaStream_t st)
 {
-    if (n > 1 && (!h_keys || !d_keys)) return fail(GBS_ERROR_INVALID_VALUE, "NULL buffer");
+    const bool pairs = h_vals != nullptr;
+    if (n > 1 && (!h_keys || !d_keys || (pairs && !d_vals))) return fail(GBS_ERROR_INVALID_VALUE, "NULL buffer");
     if (n == 0) return GBS_SUCCESS;
-    size_t need = 0;
-    gbs_status_t r = gbs_sort_keys_workspace_size(n, &need);
+    const int kind = pairs ? KIND_PAIRS : KIND_KEYS;
+    Plan P;
+    gbs_status_t r = make_plan(n, kind, nullptr, P);
     if (r) return r;
-    if (ws_bytes < need) return fail(GBS_ERROR_WORKSPACE_TOO_SMALL, "workspace %zu < %zu bytes", ws_bytes, need);
-    cudaStream_t st = (cudaStream_t)stream;
-    if (GBS_HOST_PIPE && n >= ((size_t)HP_CHUNK_TILES << 15)) {
-        // pipelined: copies overlap Step 2 (chunks of sublists) and Step 9 (bucket groups)
-        Plan P;
-        r = make_plan(n, KIND_KEYS, nullptr, P);
-        if (r) return r;
+    if (ws_bytes < P.ws) return fail(GBS_ERROR_WORKSPACE_TOO_SMALL, "workspace %zu < %zu bytes", ws_bytes, P.ws);
+    const size_t bytes = n * 4;
+    if (GBS_HOST_PIPE && !P.nodes.empty() && !P.nodes[0].leaf && P.nodes[0].B == 1 &&
+        n >= (size_t)HP_CHUNK_TILES * P.nodes[0].L) {
         const Node& top = P.nodes[0];
         cudaStream_t cin = side_stream(1), cout = side_stream(2);
-        if (!top.leaf && top.step9 < 0 && top.B == 1 && cin && cout) {
+        if (cin && cout) {
             r = check_device();
             if (r) return r;
             if (!d_ws || ((uintptr_t)d_ws & 255)) return fail(GBS_ERROR_INVALID_VALUE, "workspace NULL or not 256-byte aligned");
-            if (((uintptr_t)d_keys & 3)) return fail(GBS_ERROR_INVALID_VALUE, "keys must be 4-byte aligned");
+            if (((uintptr_t)d_keys & 3) || (pairs && ((uintptr_t)d_vals & 3)))
+                return fail(GBS_ERROR_INVALID_VALUE, "keys/values must be 4-byte aligned");
+            if (pairs) {
+                const uintptr_t k0 = (uintptr_t)d_keys, k1 = k0 + bytes, v0 = (uintptr_t)d_vals, v1 = v0 + bytes;
+                if (k0 < v1 && v0 < k1) return fail(GBS_ERROR_INVALID_VALUE, "keys and values overlap");
+            }
             char* w = reinterpret_cast<char*>(d_ws);
-            Bufs bf{d_keys, (void*)(w + top.o_reloc), d_keys, nullptr, nullptr, nullptr};
+            Bufs bf{d_keys, (void*)(w + top.o_reloc), d_keys, d_vals,
+                    pairs ? reinterpret_cast<uint32_t*>(w + top.o_reloc_v) : nullptr, d_vals};
             Probs pr{nullptr, nullptr, 0, (uint32_t)n};
-            HostPipe hp{h_keys, n, cin, cout};
-            return exec(P, 0, w, bf, pr, st, 0, &hp);
+            HostPipe hp{h_keys, h_vals, n, cin, cout};
+            r = exec(P, 0, w, bf, pr, st, 0, &hp);
+            if (r) return r;
+            if (top.step9 >= 0) {   // nested Step 9: the output is final when the level is
+                GBS_CUDA(cudaMemcpyAsync(h_keys, d_keys, bytes, cudaMemcpyDeviceToHost, st));
+                if (pairs) GBS_CUDA(cudaMemcpyAsync(h_vals, d_vals, bytes, cudaMemcpyDeviceToHost, st));
+            }
+            return GBS_SUCCESS;
         }
     }
-    GBS_CUDA(cudaMemcpyAsync(d_keys, h_keys, n * 4, cudaMemcpyHostToDevice, st));
-    r = run_sort(d_keys, nullptr, n, nullptr, 0, d_ws, ws_bytes, st);
+    GBS_CUDA(cudaMemcpyAsync(d_keys, h_keys, bytes, cudaMemcpyHostToDevice, st));
+    if (pairs) GBS_CUDA(cudaMemcpyAsync(d_vals, h_vals, bytes, cudaMemcpyHostToDevice, st));
+    r = run_sort(d_keys, d_vals, n, nullptr, 0, d_ws, ws_bytes, st);
     if (r) return r;
-    GBS_CUDA(cudaMemcpyAsync(h_keys, d_keys, n * 4, cudaMemcpyDeviceToHost, st));
+    GBS_CUDA(cudaMemcpyAsync(h_keys, d_keys, bytes, cudaMemcpyDeviceToHost, st));
+    if (pairs) GBS_CUDA(cudaMemcpyAsync(h_vals, d_vals, bytes, cudaMemcpyDeviceToHost, st));
     return GBS_SUCCESS;
+}
+
+gbs_status_t gbs_sort_keys_host(uint32_t* h_keys, size_t n, uint32_t* d_keys, void* d_ws, size_t ws_bytes,
+                                gbs_stream_t stream)
+{
+    return run_sort_host(h_keys, nullptr, n, d_keys, nullptr, d_ws, ws_bytes, (cudaStream_t)stream);
+}
+
+gbs_status_t gbs_sort_pairs_host(uint32_t* h_keys, uint32_t* h_vals, size_t n, uint32_t* d_keys, uint32_t* d_vals,
+                                 void* d_ws, size_t ws_bytes, gbs_stream_t stream)
+{
+    if (n > 1 && !h_vals) return fail(GBS_ERROR_INVALID_VALUE, "h_vals is NULL");
+    return run_sort_host(h_keys, n > 1 ? h_vals : nullptr, n, d_keys, d_vals, d_ws, ws_bytes, (cudaStream_t)stream);
 }
 
 }  // extern "C"

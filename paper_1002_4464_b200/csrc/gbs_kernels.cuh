@@ -446,9 +446,6 @@ __global__ void __launch_bounds__(BLOCK, 1) k_local_sort(LevelDev lv)
     }
 }
 
-#ifndef GBS_PAIR_PREFETCH
-#define GBS_PAIR_PREFETCH 0   // CTA-pair local sort: next half into registers during the write-back (measured slower: spills)
-#endif
 // ------------------------------------------------------------ Steps 2 + 3 on a CTA pair
 // SURVEY NEXT-2 (the B200 reading of "n/m is the shared memory size"): a
 // sublist of L = 2 tiles is sorted by a thread-block cluster of two CTAs.  Each CTA sorts
@@ -477,7 +474,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BLOCK, 1) k_local_so
     const uint32_t ntiles = lv.tile_hi ? lv.tile_hi : lv.B * lv.m;
     const uint32_t ncl = gridDim.x / 2;
     T x[ITEMS];
-    bool have = false;                                  // x already holds this sublist's half
     for (uint32_t tile = lv.tile_lo + blockIdx.x / 2; tile < ntiles; tile += ncl) {   // uniform in the pair
         uint64_t start = 0;
         int v = 0;
@@ -490,7 +486,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BLOCK, 1) k_local_so
             const int nr = max(0, min(nv - rank * H, H));
             if (nr > 0) prefetch_l2(reinterpret_cast<const T*>(lv.in) + ns + (uint64_t)rank * H, (size_t)nr * 4);
         }
-        if (!have) S::load_regs(x, lv.in, nullptr, start + (uint64_t)rank * H, vr, smem_raw);
+        S::load_regs(x, lv.in, nullptr, start + (uint64_t)rank * H, vr, smem_raw);
         CS::sort(x, sm, vr);                            // positions >= vr read as TMAX
         cluster.sync();                                 // both halves sorted and visible
         const T* peer = cluster.map_shared_rank(sm, rank ^ 1);
@@ -546,15 +542,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BLOCK, 1) k_local_so
 #pragma unroll
         for (int k = 0; k < ITEMS; ++k) sm[CS::phys((int)threadIdx.x * ITEMS + k)] = x[k];
         __syncthreads();
-        // the next sublist's half is loaded into the free registers now, in flight
-        // during the write-back (software pipelining, as k_local_sort)
-        have = GBS_PAIR_PREFETCH && tile + ncl < ntiles;
-        if (have) {
-            uint64_t nstart;
-            int nv;
-            sublist_of(lv, tile + ncl, nstart, nv);
-            S::load_regs(x, lv.in, nullptr, nstart + (uint64_t)rank * H, max(0, min(nv - rank * H, H)), smem_raw);
-        }
+        // (loading the next half into registers during the write-back, as k_local_sort
+        // does, measured slower here: it spills)
         if (vr > 0) S::store(lv.srt, nullptr, start + (uint64_t)rank * H, vr, smem_raw);
         // Step 3: samples k whose position (k+1)d - 1 falls in this CTA's half
         const uint32_t i = tile % lv.m, b = tile / lv.m;
@@ -1373,9 +1362,6 @@ __global__ void __launch_bounds__(256) k_bucket_tiers(LevelDev lv, uint32_t* lis
     if (t >= 0) lists[(uint64_t)t * count + wbase[t][w] + mine] = idx;
 }
 
-#ifndef GBS_GATHER_PF
-#define GBS_GATHER_PF 0   // fused Step 8+9: L2 prefetch of the next wave's runs (measured: no gain)
-#endif
 // Fused Step 8+9: lrel / pex staging area behind the CTA's largest tile
 template <int KIND, int BLOCK, int ITEMS>
 __host__ __device__ constexpr size_t gather_smem_offset()
@@ -1407,22 +1393,7 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK <= 576 ? 2 : 1)) k_segment_sort(
         int v;
         segment_of<MODE_BUCKET>(lv, idx, off, v);
         if (v <= 0 || (!lv.tier_list && ((uint32_t)v <= lv.seg_min || (uint32_t)v > lv.seg_max))) return;
-        {
-            // L2 prefetch of the runs of the bucket pf_stride CTAs ahead (the next wave):
-            // one bulk prefetch per run, from that bucket's a and P_i,j-1 columns
-            const uint32_t q2 = blockIdx.x + lv.pf_stride;
-            const uint32_t len = lv.tier_list ? *lv.tier_len : lv.B * lv.s;
-            if (GBS_GATHER_PF && q2 < len) {
-                const uint32_t idx2 = lv.tier_list ? lv.tier_list[q2] : q2;
-                const uint32_t b2 = idx2 / lv.s, j2 = idx2 % lv.s;
-                const uint64_t c2 = (uint64_t)b2 * lv.m * lv.s + j2;
-                const KeyT* s2 = reinterpret_cast<const KeyT*>(lv.srt) + lv.pr.offset(b2);
-                for (uint32_t i = threadIdx.x; i < lv.m; i += BLOCK) {
-                    const uint32_t n2 = lv.a[c2 + (uint64_t)i * lv.s];
-                    if (n2) prefetch_l2(s2 + (uint64_t)i * lv.L + lv.pex[c2 + (uint64_t)i * lv.s], (size_t)n2 * sizeof(KeyT));
-                }
-            }
-        }
+        // (an L2 prefetch of the next wave's runs measured no gain here)
         const uint32_t b = idx / lv.s, j = idx % lv.s;
         uint2* run = reinterpret_cast<uint2*>(smem_raw + gather_smem_offset<KIND, BLOCK, ITEMS>());
         const uint64_t col0 = (uint64_t)b * lv.m * lv.s + j;          // (row 0, column j) of problem b

@@ -16,8 +16,9 @@ for spec in args:
     lib = f"/tmp/libgbs_{name}.so"
     _build.build(out=lib, defines=d)
     for rep in range(2):
-        r = subprocess.run([sys.executable, "bench.py", "--steps", "20", "--warmup", "3", "--no-cpu-baseline"] + bench_args,
-                           capture_output=True, text=True, env=dict(os.environ, GBS_LIB=lib), cwd=ROOT)
+        r = subprocess.run([sys.executable, "bench.py", "--lib", lib, "--steps", "20", "--warmup", "3", "--no-cpu-baseline",
+                            "--no-e2e", "--no-extras"] + bench_args,
+                           capture_output=True, text=True, cwd=ROOT)
         try:
             j = json.loads(r.stdout.strip().splitlines()[-1])
             st = {k.split()[0] + ("" if "(" not in k else k[k.index("("):k.index(")") + 1]): v["ms"] for k, v in j["steps_breakdown"].items()}

@@ -1,4 +1,4 @@
-// cta_radix.cuh -- on-chip LSD radix sort of one tile (<= BLOCK*ITEMS u32 keys, or u32
+// cta_radix.cuh (prototype, measured and rejected: profiles/r02/radix_ab.md) -- on-chip LSD radix sort of one tile (<= BLOCK*ITEMS u32 keys, or u32
 // key -> u32 value pairs, stable) by one CTA.
 //
 // Steps 2 and 9 of Alg. 1 sort a sublist / bucket on one SM.  The

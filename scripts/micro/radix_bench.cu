@@ -7,7 +7,7 @@
 #include <vector>
 #include <cuda_runtime.h>
 #include "../../paper_1002_4464_b200/csrc/gbs_kernels.cuh"
-#include "../../paper_1002_4464_b200/csrc/cta_radix.cuh"
+#include "cta_radix.cuh"
 using namespace gbs;
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s at %d\n", cudaGetErrorString(e), __LINE__); exit(1); } } while (0)

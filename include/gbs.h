@@ -144,14 +144,19 @@ gbs_status_t gbs_debug_layout(size_t n, int pairs, const gbs_config_t* cfg, gbs_
 gbs_status_t gbs_sort_ex(uint32_t* d_keys, uint32_t* d_vals, size_t n, const gbs_config_t* cfg,
                          int stop_after_step, void* d_ws, size_t ws_bytes, gbs_stream_t stream);
 
-/* Per-step device time of level 1 (CUDA events recorded on the call's stream between
- * the steps' launches) for every complete sort this thread enqueues between begin and
- * end.  ms[2] = Steps 2-3 (local sort + local sampling), ms[4] = Step 4 (sample sort),
- * ms[5..8] = Steps 5-8, ms[9] = Step 9 (bucket sort or nested level); summed over
- * `calls` sorts.  gbs_profile_end synchronises the recorded events. */
+/* Per-step device time (CUDA events recorded on the call's stream between the steps'
+ * launches; the Fig. 4 breakdown) for every complete sort this thread
+ * enqueues between begin and end.  ms[2] = Steps 2-3 (local sort + local sampling),
+ * ms[4] = Step 4 (sample sort), ms[5..8] = Steps 5-8, ms[9] = Step 9 (bucket sort, or
+ * the whole nested level) of the top level, summed over `calls` sorts; ms_level[k][.]
+ * the same for level k (k = 0 top, k >= 1 the k-th nested Step 9 level, whose steps run
+ * over all buckets of the level above at once), `levels` of them.
+ * gbs_profile_end synchronises the recorded events. */
 typedef struct {
     float ms[10];
     int calls;
+    int levels;
+    float ms_level[GBS_MAX_LEVELS][10];
 } gbs_step_times_t;
 gbs_status_t gbs_profile_begin(void);
 gbs_status_t gbs_profile_end(gbs_step_times_t* out);
@@ -160,62 +165,86 @@ const char* gbs_status_string(gbs_status_t s);
 const char* gbs_last_error(void); /* thread-local */
 
 /* ------------------------------------------------------------ multi GPU */
-/* One process per GPU; a collective over all ranks of `comm` (DESIGN.md 7,
- * SURVEY 8(e)): every rank sorts its shard with the single-GPU path (E1), takes
- * s_r regular samples (E2), allgathers them (E3, NCCL), sorts them and picks p
- * splitters identically on every rank (E4-E5), cuts its sorted shard (E6),
- * allgathers the p x p counts (E7), exchanges buckets with grouped send/recv over
- * NVLink (E8) and merges the p sorted runs it received (E9, gbs_merge_runs). */
+/* One process per GPU; a collective over all ranks of `comm`:
+ * Alg. 1 once more as an outer level with one sublist per rank.  Every rank sorts its
+ * shard with the single-GPU path (E1, the outer Step 2), takes s_r regular samples (E2,
+ * Step 3), every rank receives all samples (E3), sorts them identically and picks the p
+ * splitters G_k = sorted[(k+1) s_r - 1] (E4-E5, Steps 4-5), counts for every sorted
+ * sample how many of its items are <= it (E6, Step 6), every rank receives that p x p s_r
+ * matrix F (E7, Step 7), the buckets are relocated straight into their owners' receive
+ * buffers at offsets derived from F (E8: the relocation of P:235-239 as the exchange) and
+ * every rank merges the p sorted runs it received in one pass (E9, Step 9).
+ * Transport: NVLink peer memory -- the communicator maps every rank's window (receive
+ * buffer, sample slots, F, barrier flags) into every peer with CUDA IPC and E3/E7/E8 are
+ * stores from the library's kernels into the peers' windows, ordered by device-side
+ * barriers; where a peer cannot be mapped (or gbs_comm_set_exchange(comm, 1)), NCCL
+ * allgathers and grouped send/recv carry the same data. */
 typedef struct gbs_comm* gbs_comm_t;
 #define GBS_UNIQUE_ID_BYTES 128 /* == sizeof(ncclUniqueId) */
 
 gbs_status_t gbs_get_unique_id(uint8_t id[GBS_UNIQUE_ID_BYTES]);
-/* Uses the current CUDA device.  Collective: every rank calls it with the same id. */
+/* Uses the current CUDA device.  Collective: every rank calls it with the same id.  At
+ * most 16 ranks.  The communicator owns device memory: NCCL's, a 64 KB scratch and (from
+ * the first multi-rank sort on) the peer-mapped window, sized for the largest n_local
+ * sorted so far (~4.1 n_local + 8 p^2 s_r bytes). */
 gbs_status_t gbs_comm_init(gbs_comm_t* comm, const uint8_t id[GBS_UNIQUE_ID_BYTES], int nranks,
                            int rank);
+/* Exchange transport: 0 = peer memory when every peer maps (default), 1 = NCCL.
+ * Collective (every rank sets the same mode). */
+gbs_status_t gbs_comm_set_exchange(gbs_comm_t comm, int mode);
 gbs_status_t gbs_comm_destroy(gbs_comm_t comm);
 
-/* out_capacity = n_local + (p-1)(n_local/s_r - 1): the tight receive bound. */
+/* ws_bytes: the rank's local workspace; out_capacity = n_local + (p-1)(n_local/s_r - 1),
+ * the tight receive bound (s_r = the largest power of two <= 1024 dividing n_local;
+ * out_capacity = n_local when nranks = 1).  N = nranks * n_local <= 2^32. */
 gbs_status_t gbs_sort_keys_dist_workspace_size(size_t n_local, int nranks, size_t* ws_bytes,
                                                size_t* out_capacity);
 
-/* Every rank passes the same n_local (>= 2 * s_r).  d_keys (n_local keys) is sorted
- * in place locally (E1) and then read by the exchange; d_out receives this rank's
- * part of the global order, *n_out (host) its length.  Concatenating d_out[0:n_out]
- * in rank order gives sorted(concatenation of the inputs in rank order).  The call
- * synchronises `stream` once (NCCL needs host-side counts, E7). */
-gbs_status_t gbs_sort_keys_dist(gbs_comm_t comm, uint32_t* d_keys, size_t n_local,
+/* Every rank passes the same n_local (>= 2 s_r when nranks > 1).  d_in (n_local keys,
+ * device) is read only; d_out (out_capacity keys) receives this rank's part of the
+ * global order and *n_out (host) its length.  Concatenating d_out[0:n_out] in rank order
+ * gives sorted(concatenation of the inputs in rank order).  With nranks > 1 the call
+ * synchronises `stream` once, at its end (to return *n_out); nranks = 1 is the
+ * single-GPU sort of d_in into d_out (no synchronisation).  A rank that does not join
+ * makes the others fail with GBS_ERROR_NCCL after a ~20 s timeout instead of hanging. */
+gbs_status_t gbs_sort_keys_dist(gbs_comm_t comm, const uint32_t* d_in, size_t n_local,
                                 uint32_t* d_out, size_t out_capacity, size_t* n_out, void* d_ws,
                                 size_t ws_bytes, gbs_stream_t stream);
 
-/* The p-rank path of gbs_sort_keys_dist on ONE GPU, for testing: the same per-rank
- * phases (E1-E2, E4-E6, E9 kernels) run for ranks 0..p-1 in turn, and the collectives
- * (E3, E7 allgathers, E8 all-to-all) are replaced by device copies.  d_keys holds the
- * p shards back to back (p*n_local keys), d_out p regions of out_capacity keys (rank
- * k's part at d_out + k*out_capacity), n_out a host array of p lengths, d_ws p
- * workspaces of ws_bytes (per-rank size from gbs_sort_keys_dist_workspace_size).
- * Synchronises `stream` once (E7). */
-gbs_status_t gbs_sort_keys_dist_emulated(int p, uint32_t* d_keys, size_t n_local, uint32_t* d_out,
-                                         size_t out_capacity, size_t* n_out, void* d_ws,
-                                         size_t ws_bytes, gbs_stream_t stream);
+/* Phase times of the multi-GPU calls this thread enqueued between gbs_profile_begin()
+ * and this call (which ends the profile, like gbs_profile_end): ms[0] E1 local sort,
+ * ms[1] E2-E7 (samples, cuts and their exchange), ms[2] E8 exchange (incl. its barrier),
+ * ms[3] E9 merge, ms[5] the whole call; exchange_bytes = keys bytes this rank sent to
+ * other ranks; path 1 = peer memory, 2 = NCCL, 0 = one rank. */
+typedef struct {
+    float ms[6];
+    double exchange_bytes;
+    int calls;
+    int path;
+} gbs_dist_times_t;
+gbs_status_t gbs_dist_profile_end(gbs_dist_times_t* out);
 
-/* Host-only exchange plan (E7-E8), exported so the protocol can be tested without a
- * GPU.  cuts: p x p row-major, cuts[r*p + k] = cut_{r,k} (#items of rank r's sorted
- * shard <= splitter k; cuts[r*p + p-1] = n_local).  For `rank`, fills send_off/
- * send_cnt (into its shard) and recv_off/recv_cnt (into d_out, rank order) for each
- * peer, and *n_out.  Returns GBS_ERROR_INVALID_VALUE on inconsistent cuts. */
+/* The p-rank path of gbs_sort_keys_dist on ONE GPU, for testing: the same per-rank
+ * kernels (E1-E9, peer-memory transport) run for ranks 0..p-1 in turn, with the p
+ * windows as regions of the workspace and stream order in place of the barriers.
+ * d_keys holds the p shards back to back (p*n_local keys, read only), d_out p regions of
+ * out_capacity keys (rank k's part at d_out + k*out_capacity), n_out a host array of p
+ * lengths, d_ws one workspace of gbs_sort_keys_dist_emulated_workspace_size bytes
+ * (256-byte aligned).  Synchronises `stream` once. */
+gbs_status_t gbs_sort_keys_dist_emulated_workspace_size(size_t n_local, int p, size_t* bytes);
+gbs_status_t gbs_sort_keys_dist_emulated(int p, const uint32_t* d_keys, size_t n_local,
+                                         uint32_t* d_out, size_t out_capacity, size_t* n_out,
+                                         void* d_ws, size_t ws_bytes, gbs_stream_t stream);
+
+/* Host-only exchange plan (E7-E8 counts from the splitters' cuts), exported so the
+ * protocol can be tested without a GPU.  cuts: p x p row-major, cuts[r*p + k] = cut_{r,k}
+ * (#items of rank r's sorted shard <= splitter k; cuts[r*p + p-1] = n_local).  For
+ * `rank`, fills send_off/send_cnt (into its shard) and recv_off/recv_cnt (into its
+ * receive buffer, source order) for each peer, and *n_out.  GBS_ERROR_INVALID_VALUE on
+ * inconsistent cuts. */
 gbs_status_t gbs_exchange_plan(const uint64_t* cuts, int p, int rank, uint64_t* send_off,
                                uint64_t* send_cnt, uint64_t* recv_off, uint64_t* recv_cnt,
                                uint64_t* n_out);
-
-/* Merge p sorted runs of u32 keys (E9 of the multi-GPU level: the runs a rank receives,
- * one per source rank, each sorted).  d_keys[run_off[r] .. run_off[r+1]) is run r
- * (run_off: host array of p+1 offsets, run_off[0] = 0, nondecreasing, run_off[p] = n);
- * on return d_keys[0..n) is sorted (in place; ties keep run order).  A pairwise merge-path
- * tree: ceil(log2 p) passes through the workspace.  p <= 64. */
-gbs_status_t gbs_merge_runs_workspace_size(size_t n, int p, size_t* bytes);
-gbs_status_t gbs_merge_runs(uint32_t* d_keys, const uint64_t* run_off, int p, void* d_ws, size_t ws_bytes,
-                            gbs_stream_t stream);
 
 #ifdef __cplusplus
 }

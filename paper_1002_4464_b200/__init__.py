@@ -18,7 +18,7 @@ import os
 
 __all__ = ["lib", "GbsError", "plan", "workspace_size", "debug_layout", "sort_keys", "sort_pairs",
            "sort_ex", "sort_keys_host", "sort_pairs_host", "Workspace", "get_unique_id", "Comm", "sort_keys_dist",
-           "exchange_plan", "dist_workspace_size"]
+           "exchange_plan", "dist_workspace_size", "dist_profile_end", "sort_keys_dist_emulated"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libgbs.so")
@@ -42,7 +42,12 @@ class PlanT(C.Structure):
 
 
 class StepTimes(C.Structure):
-    _fields_ = [("ms", C.c_float * 10), ("calls", C.c_int)]
+    _fields_ = [("ms", C.c_float * 10), ("calls", C.c_int), ("levels", C.c_int),
+                ("ms_level", (C.c_float * 10) * MAX_LEVELS)]
+
+
+class DistTimes(C.Structure):
+    _fields_ = [("ms", C.c_float * 6), ("exchange_bytes", C.c_double), ("calls", C.c_int), ("path", C.c_int)]
 
 
 class LayoutT(C.Structure):
@@ -82,8 +87,9 @@ def lib():
             "gbs_exchange_plan": [p, C.c_int, C.c_int, p, p, p, p, p],
             "gbs_profile_begin": [],
             "gbs_profile_end": [C.POINTER(StepTimes)],
-            "gbs_merge_runs_workspace_size": [sz, C.c_int, C.POINTER(sz)],
-            "gbs_merge_runs": [p, p, C.c_int, p, sz, p],
+            "gbs_comm_set_exchange": [p, C.c_int],
+            "gbs_dist_profile_end": [p],
+            "gbs_sort_keys_dist_emulated_workspace_size": [sz, C.c_int, C.POINTER(sz)],
         }
         for name, args in sigs.items():
             f = getattr(L, name)
@@ -142,11 +148,13 @@ def profile_begin():
 
 
 def profile_end() -> dict:
-    """{step: total ms} over the sorts enqueued since profile_begin(), and 'calls'."""
+    """{step: total ms} of the top level over the sorts enqueued since profile_begin(),
+    'calls', and 'level' = a list of such dicts per level (0 = top, k = k-th nested Step 9)."""
     out = StepTimes()
     _check(lib().gbs_profile_end(C.byref(out)))
     d = {k: out.ms[k] for k in (2, 4, 5, 6, 7, 8, 9)}
     d["calls"] = out.calls
+    d["level"] = [{k: out.ms_level[l][k] for k in (2, 4, 5, 6, 7, 8, 9)} for l in range(out.levels)]
     return d
 
 
@@ -341,20 +349,6 @@ def sort_pairs_host(h_keys, h_vals, d_keys, d_vals, ws: Workspace | None = None,
     return h_keys, h_vals
 
 
-def merge_runs(keys, run_off, ws: Workspace | None = None, stream=None):
-    """Merge sorted runs keys[run_off[r]:run_off[r+1]] in place (E9 of the multi-GPU level)."""
-    import numpy as np
-    off = np.ascontiguousarray(run_off, dtype=np.uint64)
-    p = off.size - 1
-    kp = _dev_ptr(keys, "keys")
-    need = C.c_size_t()
-    _check(lib().gbs_merge_runs_workspace_size(int(off[-1]), p, C.byref(need)))
-    with _On(keys.device, stream) as on:
-        wp, wb = on.ws(need.value, ws)
-        _check(lib().gbs_merge_runs(C.c_void_p(kp), off.ctypes.data_as(C.c_void_p), p, wp, wb, on.s))
-    return keys
-
-
 # ----------------------------------------------------------------- multi GPU
 
 def get_unique_id() -> bytes:
@@ -382,9 +376,10 @@ def exchange_plan(cuts, rank: int):
 
 
 class Comm:
-    """NCCL communicator of libgbs, bootstrapped over a torch.distributed group."""
+    """libgbs communicator (NCCL + peer-mapped windows), bootstrapped over a
+    torch.distributed group: rank 0 creates the NCCL unique id, the group broadcasts it."""
 
-    def __init__(self, group=None):
+    def __init__(self, group=None, exchange: str = "p2p"):
         import torch.distributed as dist
         self.rank = dist.get_rank(group)
         self.nranks = dist.get_world_size(group)
@@ -395,6 +390,12 @@ class Comm:
         h = C.c_void_p()
         _check(lib().gbs_comm_init(C.byref(h), idbuf, self.nranks, self.rank))
         self.handle = h
+        if exchange != "p2p":
+            self.set_exchange(exchange)
+
+    def set_exchange(self, exchange: str):
+        """'p2p' (peer memory, default) or 'nccl'; collective."""
+        _check(lib().gbs_comm_set_exchange(self.handle, {"p2p": 0, "nccl": 1}[exchange]))
 
     def close(self):
         if self.handle:
@@ -403,8 +404,8 @@ class Comm:
 
 
 def sort_keys_dist(keys, comm: Comm, out=None, ws: Workspace | None = None, stream=None):
-    """Every rank passes an equal-length shard; ``keys`` is sorted locally in place and
-    the rank's part of the global order is returned (a view of ``out``)."""
+    """Every rank passes an equal-length shard (read only); returns the rank's part of the
+    global order (a view of ``out``, allocated if missing or too small)."""
     torch = _torch()
     n = keys.numel()
     kp = _dev_ptr(keys, "keys")
@@ -419,20 +420,34 @@ def sort_keys_dist(keys, comm: Comm, out=None, ws: Workspace | None = None, stre
     return out[:n_out.value]
 
 
+def dist_profile_end() -> dict:
+    """Phase times (ms, summed over the calls) of the multi-GPU sorts since profile_begin()."""
+    out = DistTimes()
+    _check(lib().gbs_dist_profile_end(C.byref(out)))
+    names = ["local_sort_ms", "samples_cuts_ms", "exchange_ms", "merge_ms", "_", "total_ms"]
+    c = max(out.calls, 1)
+    d = {nm: out.ms[i] / c for i, nm in enumerate(names) if nm != "_"}
+    d.update(calls=out.calls, exchange_bytes=out.exchange_bytes / c,
+             path={0: "one rank", 1: "peer memory (NVLink stores)", 2: "nccl"}.get(out.path))
+    return d
+
+
 def sort_keys_dist_emulated(shards, p: int, stream=None):
-    """Testing aid: the p-rank multi-GPU path on one GPU (collectives replaced by device
-    copies).  ``shards``: p*n_local keys, rank r's shard at [r n_local, (r+1) n_local)
-    (sorted locally in place).  Returns the list of the p ranks' parts."""
+    """Testing aid: the p-rank multi-GPU path on one GPU (the same kernels, the p windows
+    as regions of one workspace).  ``shards``: p*n_local keys, rank r's shard at
+    [r n_local, (r+1) n_local) (read only).  Returns the list of the p ranks' parts."""
     torch = _torch()
     assert shards.numel() % p == 0
     n = shards.numel() // p
     kp = _dev_ptr(shards, "shards")
-    need, cap = dist_workspace_size(n, p)
+    _, cap = dist_workspace_size(n, p)
+    tot = C.c_size_t()
+    _check(lib().gbs_sort_keys_dist_emulated_workspace_size(n, p, C.byref(tot)))
     out = torch.empty(p * cap, dtype=shards.dtype, device=shards.device)
-    ws = torch.empty(p * need + 256, dtype=torch.uint8, device=shards.device)
-    wp = (ws.data_ptr() + 255) // 256 * 256
     n_out = (C.c_size_t * p)()
     with _On(shards.device, stream) as on:
+        ws = torch.empty(tot.value + 256, dtype=torch.uint8, device=shards.device)
+        wp = (ws.data_ptr() + 255) // 256 * 256
         _check(lib().gbs_sort_keys_dist_emulated(p, C.c_void_p(kp), n, C.c_void_p(out.data_ptr()), cap, n_out,
-                                                 C.c_void_p(wp), need, on.s))
+                                                 C.c_void_p(wp), tot.value, on.s))
     return [out[r * cap:r * cap + n_out[r]] for r in range(p)]

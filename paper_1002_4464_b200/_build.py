@@ -7,7 +7,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libgbs.so")
-SOURCES = ["gbs_api.cu", "gbs_dist.cu", "gbs_merge.cu"]
+SOURCES = ["gbs_api.cu", "gbs_dist.cu"]
 DEPS = SOURCES + ["gbs_kernels.cuh", "cta_sort.cuh", "gbs_internal.h", "../../include/gbs.h"]
 
 

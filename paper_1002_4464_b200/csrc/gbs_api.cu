@@ -12,6 +12,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
 #include <mutex>
 #include <type_traits>
 #include <vector>
@@ -62,7 +63,11 @@ static bool debug_sync()
 // ----------------------------------------------------------------- step profiling
 // Per-step CUDA events on the call's stream for the top level (gbs_profile_begin/end).
 static thread_local bool g_prof = false;
-static thread_local std::vector<std::array<cudaEvent_t, 8>> g_prof_calls;
+struct ProfCall {
+    int level;                       // 0 = top level, k = k-th nested Step 9 level
+    std::array<cudaEvent_t, 8> ev;
+};
+static thread_local std::deque<ProfCall> g_prof_calls;   // deque: stable element addresses
 
 struct ProfMarks {
     cudaEvent_t* ev = nullptr;
@@ -132,6 +137,7 @@ struct Node {
     bool fuse89 = false;  // Step 9 gathers straight from the sorted sublists (no Step 8 pass)
     bool s4_tree = false; // Step 4 as a merge tree (R22) instead of a u64 level
     int s4_levels = 0;    // its global merge levels (between the tile merge and the selection)
+    int level = 0;        // 0 top, k nested Step 9 level k, -1 a Step 4 sample level (profiling)
     size_t o_s4tmp = 0;   // its ping-pong buffer (m*s u64)
 };
 
@@ -234,7 +240,7 @@ static int reloc_launches(int kind);   // Step 8: 1, or 2 when both relocation f
 
 // Returns node index, or -1 with g_err set.
 static int build_node(Plan& P, int kind, uint32_t B, uint64_t N, uint32_t pad_base, const gbs_config_t* cfg,
-                      bool own_reloc)
+                      bool own_reloc, int level = 0)
 {
     const uint32_t tile = tile_of(kind);
     Node nd;
@@ -242,6 +248,7 @@ static int build_node(Plan& P, int kind, uint32_t B, uint64_t N, uint32_t pad_ba
     nd.B = B;
     nd.N = N;
     nd.pad_base = pad_base;
+    nd.level = level;
     const bool use_cfg = cfg && cfg->L;
     if (!use_cfg && N <= tile) {
         nd.leaf = true;
@@ -321,7 +328,7 @@ static int build_node(Plan& P, int kind, uint32_t B, uint64_t N, uint32_t pad_ba
         for (uint64_t R = S4_TILE; 2 * R < ms; R *= 2) ++me.s4_levels;
         P.launches += 2 + me.s4_levels;
     } else {
-        const int c4 = build_node(P, KIND_U64, B, (uint64_t)nd.m * s, child_pad, nullptr, true);
+        const int c4 = build_node(P, KIND_U64, B, (uint64_t)nd.m * s, child_pad, nullptr, true, -1);
         if (c4 < 0) return -1;
         P.nodes[idx].step4 = c4;
     }
@@ -349,7 +356,7 @@ static int build_node(Plan& P, int kind, uint32_t B, uint64_t N, uint32_t pad_ba
         P.launches += reloc_launches(kind) + 1;  // relocate + child descriptors
         const uint64_t nb = (uint64_t)B * s;
         if (nb >= (1ull << 31)) { snprintf(g_err, sizeof g_err, "too many nested problems"); return -1; }
-        const int c9 = build_node(P, kind, (uint32_t)nb, nd.hi, child_pad, nullptr, false);
+        const int c9 = build_node(P, kind, (uint32_t)nb, nd.hi, child_pad, nullptr, false, level >= 0 ? level + 1 : -1);
         if (c9 < 0) return -1;
         P.nodes[idx].step9 = c9;
     }
@@ -647,6 +654,9 @@ constexpr uint32_t HP_GROUPS = 16;        // Step 9 bucket groups (D2H chunks)
 struct Bufs {
     void *in, *reloc, *out;
     uint32_t *in_v, *reloc_v, *out_v;
+    // out-of-place sorts (keys): where Step 2 writes the sorted sublists (in stays
+    // read-only); null = in place (in)
+    void* srt = nullptr;
 };
 
 template <int KIND>
@@ -827,21 +837,20 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
     // bucket CTAs would overwrite runs other CTAs still gather), so it writes the sorted
     // sublists to the reloc buffer, which Step 8 no longer needs
     const bool fuse = nd.fuse89 && stop == 0 && !hp;
-    lv.srt = lv.in;
+    lv.srt = bf.srt ? bf.srt : lv.in;
     lv.srt_v = lv.in_v;
     lv.pex = reinterpret_cast<uint32_t*>(ws + nd.o_pex);
-    if (fuse) {
-        if (lv.in == lv.out) {
-            lv.srt = lv.reloc;
-            lv.srt_v = lv.reloc_v;
-        }
+    if (fuse && lv.srt == lv.out) {
+        lv.srt = lv.reloc;
+        lv.srt_v = lv.reloc_v;
     }
     ProfMarks pm;
-    if (g_prof && ni == 0 && stop == 0) {
-        std::array<cudaEvent_t, 8> evs;
-        for (auto& e : evs) cudaEventCreate(&e);
-        g_prof_calls.push_back(evs);
-        pm.ev = g_prof_calls.back().data();
+    if (g_prof && nd.level >= 0 && nd.level < GBS_MAX_LEVELS && stop == 0) {
+        ProfCall pc;
+        pc.level = nd.level;
+        for (auto& e : pc.ev) cudaEventCreate(&e);
+        g_prof_calls.push_back(pc);
+        pm.ev = g_prof_calls.back().ev.data();
         pm.st = st;
     }
     pm.mark();
@@ -987,7 +996,9 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
         const uint64_t tot = (uint64_t)nd.B * nd.s;
         launch_k(k_child_desc, (unsigned)((tot + 255) / 256), 256, 0, st, lv);
         GBS_LAUNCHED();
-        Bufs b9{bf.reloc, bf.in, bf.out, bf.reloc_v, bf.in_v, bf.out_v};
+        // the nested level sorts its problems in place in the reloc buffer and uses the
+        // sublists' buffer (dead after Step 8) as its own relocation target
+        Bufs b9{bf.reloc, bf.srt ? bf.srt : bf.in, bf.out, bf.reloc_v, bf.in_v, bf.out_v};
         Probs p9{lv.child_off, lv.child_len, 0, 0};
         gbs_status_t r = exec(P, nd.step9, ws, b9, p9, st, 0);
         if (r) return r;
@@ -1066,6 +1077,44 @@ gbs_status_t sort_u64_inplace(unsigned long long* d, size_t n, void* ws, size_t 
     return exec(P, 0, w, bf, pr, st, 0);
 }
 
+// Out-of-place keys sort (the multi-GPU entry's local sort, E1): in[0, n) is only read;
+// Step 2 writes the sorted sublists to a workspace buffer of n keys behind the plan's
+// workspace, and the result lands in out (no extra pass).
+gbs_status_t sort_keys_oop_ws(size_t n, size_t* bytes)
+{
+    Plan P;
+    gbs_status_t r = make_plan(n, KIND_KEYS, nullptr, P);
+    if (r) return r;
+    *bytes = P.ws + (n * 4 + 255) / 256 * 256;
+    return GBS_SUCCESS;
+}
+
+gbs_status_t sort_keys_oop(const uint32_t* in, uint32_t* out, size_t n, void* ws, size_t ws_bytes, cudaStream_t st)
+{
+    Plan P;
+    gbs_status_t r = make_plan(n, KIND_KEYS, nullptr, P);
+    if (r) return r;
+    if (n == 0) return GBS_SUCCESS;
+    if (!in || !out || ((uintptr_t)in & 3) || ((uintptr_t)out & 3)) return fail(GBS_ERROR_INVALID_VALUE, "oop sort: bad buffers");
+    if (n == 1) {
+        GBS_CUDA(cudaMemcpyAsync(out, in, 4, cudaMemcpyDeviceToDevice, st));
+        return GBS_SUCCESS;
+    }
+    const size_t need = P.ws + (n * 4 + 255) / 256 * 256;
+    if (ws_bytes < need) return fail(GBS_ERROR_WORKSPACE_TOO_SMALL, "workspace %zu < %zu bytes", ws_bytes, need);
+    if (!ws || ((uintptr_t)ws & 255)) return fail(GBS_ERROR_INVALID_VALUE, "workspace NULL or not 256-byte aligned");
+    r = check_device();
+    if (r) return r;
+    char* w = reinterpret_cast<char*>(ws);
+    const Node& top = P.nodes[0];
+    Bufs bf{const_cast<uint32_t*>(in), top.leaf ? (void*)out : (void*)(w + top.o_reloc), out, nullptr, nullptr, nullptr};
+    bf.srt = w + P.ws;
+    Probs pr{nullptr, nullptr, 0, (uint32_t)n};
+    return exec(P, 0, w, bf, pr, st, 0);
+}
+
+bool profiling() { return g_prof; }
+
 }  // namespace gbs
 
 using namespace gbs;
@@ -1085,16 +1134,20 @@ gbs_status_t gbs_profile_end(gbs_step_times_t* out)
     g_prof = false;
     if (out) memset(out, 0, sizeof *out);
     gbs_status_t rc = GBS_SUCCESS;
-    for (auto& evs : g_prof_calls) {
-        if (cudaEventSynchronize(evs[7]) != cudaSuccess) rc = fail(GBS_ERROR_CUDA, "profile event sync failed");
+    for (auto& pc : g_prof_calls) {
+        if (cudaEventSynchronize(pc.ev[7]) != cudaSuccess) rc = fail(GBS_ERROR_CUDA, "profile event sync failed");
         static const int step_of[7] = {2, 4, 5, 6, 7, 8, 9};
         for (int k = 0; k < 7 && out && !rc; ++k) {
             float ms = 0.f;
-            cudaEventElapsedTime(&ms, evs[k], evs[k + 1]);
-            out->ms[step_of[k]] += ms;
+            cudaEventElapsedTime(&ms, pc.ev[k], pc.ev[k + 1]);
+            out->ms_level[pc.level][step_of[k]] += ms;
+            if (pc.level == 0) out->ms[step_of[k]] += ms;
         }
-        if (out && !rc) out->calls += 1;
-        for (auto e : evs) cudaEventDestroy(e);
+        if (out && !rc) {
+            if (pc.level == 0) out->calls += 1;
+            if (pc.level + 1 > out->levels) out->levels = pc.level + 1;
+        }
+        for (auto e : pc.ev) cudaEventDestroy(e);
     }
     g_prof_calls.clear();
     return rc;

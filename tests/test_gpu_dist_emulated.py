@@ -1,11 +1,13 @@
 """GPU parity of the multi-GPU path at p > 1 on ONE GPU (-m gpu).
 
-`gbs_sort_keys_dist_emulated` runs the same per-rank phases as `gbs_sort_keys_dist`
-(E1-E2 local sort + regular samples, E4-E6 sample sort + cut points, E9 p-way merge)
-for ranks 0..p-1 in turn, with the collectives (E3/E7 allgathers, E8 all-to-all)
-replaced by device copies.  Compared with the CPU oracle's PSRS outer level
+`gbs_sort_keys_dist_emulated` runs the same per-rank kernels as `gbs_sort_keys_dist`
+with the peer-memory transport -- E1 local sort, E2-E3 samples stored into every rank's
+window, E4-E7 sample sort + fine cuts stored into every window, E8 relocation of the
+runs straight into the owners' receive buffers, E9 one-pass k-way merge -- for ranks
+0..p-1 in turn, with the p windows as regions of one workspace and stream order in
+place of the device barriers.  Compared with the CPU oracle's PSRS outer level
 (oracle/gbs_oracle.c): every rank's part bit-exact, the receive counts
-equal, and the receive bound n_l + (p-1)(n_l/s_r - 1) respected."""
+equal, the receive bound n_l + (p-1)(n_l/s_r - 1) respected, the input unchanged."""
 import numpy as np
 import pytest
 
@@ -35,14 +37,12 @@ def s_r_of(n_local: int) -> int:
     return s
 
 
-@pytest.mark.parametrize("p", [2, 3, 4, 8])
-@pytest.mark.parametrize("n_local", [1 << 16, (1 << 20) + 64])
-@pytest.mark.parametrize("dist", ["uniform", "zero", "det_duplicates", "staggered", "sorted"])
-def test_dist_emulated_matches_oracle_psrs(dev, p, n_local, dist):
-    keys = gi.generate(dist, p * n_local, seed=p)
+def check_emulated(dev, p, n_local, dist, seed):
+    keys = gi.generate(dist, p * n_local, seed=seed)
     shards = torch.from_numpy(keys.view(np.int32).copy()).to(dev)
     parts = gbs.sort_keys_dist_emulated(shards, p)
     torch.cuda.synchronize()
+    assert np.array_equal(shards.cpu().numpy().view(np.uint32), keys), "input modified"
     s_r = s_r_of(n_local)
     exp, counts, _ = oracle.psrs(keys, p, s_r)
     got_counts = [t.numel() for t in parts]
@@ -51,3 +51,16 @@ def test_dist_emulated_matches_oracle_psrs(dev, p, n_local, dist):
     got = np.concatenate([t.cpu().numpy().view(np.uint32) for t in parts])
     assert np.array_equal(got, exp)
     assert np.array_equal(exp, np.sort(keys))
+
+
+@pytest.mark.parametrize("p", [2, 3, 4, 8, 16])
+@pytest.mark.parametrize("n_local", [1 << 16, (1 << 20) + 64, 3 * 4099])
+@pytest.mark.parametrize("dist", ["uniform", "zero", "det_duplicates", "staggered", "sorted", "gaussian",
+                                  "bucket_sorted"])
+def test_dist_emulated_matches_oracle_psrs(dev, p, n_local, dist):
+    check_emulated(dev, p, n_local, dist, seed=p)
+
+
+def test_dist_emulated_2_27_per_rank(dev):
+    """One case at C5-like shard size: 2^27 keys per rank, p = 2 (the oracle sorts 2^28)."""
+    check_emulated(dev, 2, 1 << 27, "uniform", seed=5)

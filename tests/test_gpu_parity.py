@@ -224,7 +224,8 @@ def test_C2_C3_full_size(dev, dist):
 
 
 def test_dist_single_rank_nccl(dev):
-    """The multi-GPU entry with p = 1 (one NCCL rank): E1-E9 run, output == sort."""
+    """The multi-GPU entry with p = 1 (one NCCL rank): the out-of-place local sort is the
+    whole job; output == sort, the input is left unchanged (read only)."""
     import ctypes as C
     L = gbs.lib()
     uid = gbs.get_unique_id()
@@ -237,9 +238,11 @@ def test_dist_single_rank_nccl(dev):
     n = 1 << 20
     keys = gi.generate("staggered", n, seed=1)
     d = to_dev(keys, dev)
-    out = gbs.sort_keys_dist(d, _C)
-    torch.cuda.synchronize()
-    assert np.array_equal(to_np(out), np.sort(keys))
+    for _ in range(2):
+        out = gbs.sort_keys_dist(d, _C)
+        torch.cuda.synchronize()
+        assert np.array_equal(to_np(out), np.sort(keys))
+        assert np.array_equal(to_np(d), keys)
     assert L.gbs_comm_destroy(h) == 0
 
 
@@ -264,23 +267,6 @@ def test_C4_pairs_full_size(dev):
     assert torch.equal(keys_in[vals.long()], keys)
     eq = k64[1:] == k64[:-1]
     assert bool((vals[1:][eq] > vals[:-1][eq]).all())
-
-
-@pytest.mark.parametrize("p,n", [(2, 1000), (3, 100_003), (8, 1 << 20), (5, 7), (64, 1 << 18), (8, 0),
-                                 (2, 4096), (7, 3 * 4096 + 1)])
-def test_merge_runs(dev, p, n):
-    """E9 building block: p sorted runs (random lengths, some empty, many duplicates)
-    merged in place == the plain definition (a library sort of the concatenation)."""
-    rng = np.random.default_rng(p * 1000 + n)
-    cuts = np.sort(rng.integers(0, n + 1, p - 1)) if p > 1 else np.array([], np.int64)
-    off = np.concatenate([[0], cuts, [n]]).astype(np.uint64)
-    keys = (rng.integers(0, 1 << 32, n, dtype=np.uint64) % (1 << 32 if p % 2 else 97)).astype(np.uint32)
-    for r in range(p):
-        keys[off[r]:off[r + 1]] = np.sort(keys[off[r]:off[r + 1]])
-    d = to_dev(keys, dev)
-    gbs.merge_runs(d, off)
-    torch.cuda.synchronize()
-    assert np.array_equal(to_np(d), np.sort(keys))
 
 
 @pytest.mark.parametrize("args", [("67108864", "32768", "64"), ("16777216", "32768", "512"),

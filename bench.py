@@ -67,6 +67,8 @@ def parse():
     ap.add_argument("--force-dist", action="store_true",
                     help="use the multi-GPU entry even with one rank (exercises E1-E9 on one GPU)")
     ap.add_argument("--lib", default=None, help="tuning only: load this libgbs build instead of the in-tree one")
+    ap.add_argument("--ncu-one", action="store_true",
+                    help="profiling only: run exactly one sort of the workload (for ncu captures) and exit")
     a = ap.parse_args()
     if a.workload is None:
         a.workload = "C5" if (a.gpus > 1 or a.force_dist) else "C4"
@@ -402,6 +404,17 @@ def main():
 
     # ---------------- headline (N = 1)
     n = args.n or w["n"]
+    if args.ncu_one:
+        keys = gi.generate_torch(args.dist, n, seed=0, device=dev)
+        vals = torch.arange(n, dtype=torch.int32, device=dev) if pairs else None
+        torch.cuda.synchronize()
+        if pairs:
+            gbs.sort_pairs(keys, vals)
+        else:
+            gbs.sort_keys(keys)
+        torch.cuda.synchronize()
+        print(json.dumps({"ncu_one": args.workload, "n": n}))
+        return
     res = run_single(args, torch, gi, gbs, dev, stream, flush, peak, n, pairs, args.dist, args.steps, args.warmup,
                      headline=True)
     unit = "pairs/s" if pairs else "keys/s"

@@ -21,7 +21,10 @@ for spec in args:
                            capture_output=True, text=True, cwd=ROOT)
         try:
             j = json.loads(r.stdout.strip().splitlines()[-1])
-            st = {k.split()[0] + ("" if "(" not in k else k[k.index("("):k.index(")") + 1]): v["ms"] for k, v in j["steps_breakdown"].items()}
+            st = {}
+            for lev, steps in (j.get("steps_breakdown") or {}).items():
+                for k, v in steps.items():
+                    st[f"{lev[-1]}:{k.split()[1]}"] = v["ms"]
             print(f"{name:14s} {j['value'] / 1e9:7.2f} G/s  {j['ms_per_step']:.4f} ms  {st}", flush=True)
         except Exception as e:  # noqa: BLE001
             print(name, "failed", e, r.stderr[-400:], flush=True)

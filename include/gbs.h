@@ -83,6 +83,22 @@ gbs_status_t gbs_sort_keys_typed(void* d_keys, size_t n, int key_type, void* d_w
 gbs_status_t gbs_sort_pairs_typed(void* d_keys, uint32_t* d_vals, size_t n, int key_type, void* d_ws,
                                   size_t ws_bytes, gbs_stream_t stream);
 
+/* 64-bit keys (the paper never fixes the item type, R1).
+ * GBS_KEY64_U64 unsigned, GBS_KEY64_I64 two's complement, GBS_KEY64_F64 IEEE-754 binary64
+ * in totalOrder (-NaN < -inf < ... < -0 < +0 < ... < +inf < +NaN).  The key's
+ * order-preserving u64 image is sorted as the composite (high half, low half) by two
+ * stable u32 passes of the pairs GBS (low half first, each with the item index as the
+ * value), then the original 8-byte keys (and the values) are gathered by the final index
+ * permutation: ascending, stable (equals std::stable_sort by numeric key).  d_keys: n
+ * 8-byte keys, 8-byte aligned, sorted in place; d_vals (pairs): n u32 values, not
+ * overlapping the keys.  Workspace from gbs_sort64_workspace_size(n, pairs).  n <= 2^31. */
+typedef enum { GBS_KEY64_U64 = 0, GBS_KEY64_I64 = 1, GBS_KEY64_F64 = 2 } gbs_key64_type_t;
+gbs_status_t gbs_sort64_workspace_size(size_t n, int pairs, size_t* bytes);
+gbs_status_t gbs_sort_keys64(void* d_keys, size_t n, int key_type, void* d_ws, size_t ws_bytes,
+                             gbs_stream_t stream);
+gbs_status_t gbs_sort_pairs64(void* d_keys, uint32_t* d_vals, size_t n, int key_type, void* d_ws,
+                              size_t ws_bytes, gbs_stream_t stream);
+
 /* End to end from HOST buffers: copy h_keys (pinned host, n keys) to d_keys, sort,
  * copy back to h_keys; all three enqueued on `stream` (H2D + sort + D2H).  Large inputs
  * are pipelined: the H2D copy is chunked by sublists so Step 2 sorts each chunk as it

@@ -170,3 +170,40 @@ def offsets(a):
 
 def composite(key: int, tag: int) -> int:
     return (int(key) << 32) | int(tag)
+
+
+# --- 64-bit keys: the plain definition of the result ---------------
+# The paper's problem statement sorts "an array A with n data items" and never
+# fixes the item type (R1).  For 64-bit keys the oracle is the definition the
+# method must reach exactly: a stable sort by the key's numeric order.
+# u64 / i64: the integer order.  f64: IEEE-754 totalOrder (IEEE 754-2008 section 5.10),
+# written out: -NaN (larger payload first) < -inf < negative finite < -0 < +0 < positive
+# finite < +inf < +NaN (larger payload last).
+
+def _f64_total_order_key(bits: int):
+    sign = bits >> 63
+    exp = (bits >> 52) & 0x7FF
+    frac = bits & ((1 << 52) - 1)
+    if exp == 0x7FF and frac:                       # NaN: ordered by sign, then payload
+        return (3, frac) if not sign else (-3, -frac)
+    value = np.array([bits], dtype=np.uint64).view(np.float64)[0]
+    zero_rank = (0 if sign else 1) if value == 0 else 0
+    return (0, float(value), zero_rank)
+
+
+def sort64(keys, vals=None, key_type: str = "uint64"):
+    """Stable sort of 64-bit keys (uint64 / int64 / float64 as raw 8-byte items) [and u32
+    values] by numeric key; pure Python ordering (small inputs).  Returns (keys, vals)."""
+    k = np.ascontiguousarray(keys)
+    bits = k.view(np.uint64)
+    if key_type == "uint64":
+        keyf = [int(b) for b in bits]
+    elif key_type == "int64":
+        keyf = [int(b) for b in bits.view(np.int64)]
+    elif key_type == "float64":
+        keyf = [_f64_total_order_key(int(b)) for b in bits]
+    else:
+        raise ValueError(key_type)
+    order = sorted(range(k.size), key=lambda i: keyf[i])        # Python's sort is stable
+    order = np.array(order, dtype=np.int64)
+    return k[order], (None if vals is None else np.ascontiguousarray(vals)[order])

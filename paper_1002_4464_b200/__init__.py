@@ -17,7 +17,7 @@ import functools
 import os
 
 __all__ = ["lib", "GbsError", "plan", "workspace_size", "debug_layout", "sort_keys", "sort_pairs",
-           "sort_ex", "sort_keys_host", "sort_pairs_host", "Workspace", "get_unique_id", "Comm", "sort_keys_dist",
+           "sort_ex", "sort_keys_host", "sort_pairs_host", "sort_keys64", "sort_pairs64", "Workspace", "get_unique_id", "Comm", "sort_keys_dist",
            "exchange_plan", "dist_workspace_size", "dist_profile_end", "sort_keys_dist_emulated"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -88,6 +88,9 @@ def lib():
             "gbs_profile_begin": [],
             "gbs_profile_end": [C.POINTER(StepTimes)],
             "gbs_comm_set_exchange": [p, C.c_int],
+            "gbs_sort64_workspace_size": [sz, C.c_int, C.POINTER(sz)],
+            "gbs_sort_keys64": [p, sz, C.c_int, p, sz, p],
+            "gbs_sort_pairs64": [p, p, sz, C.c_int, p, sz, p],
             "gbs_dist_profile_end": [p],
             "gbs_sort_keys_dist_emulated_workspace_size": [sz, C.c_int, C.POINTER(sz)],
         }
@@ -296,6 +299,52 @@ def sort_pairs_typed(keys, vals, key_type=None, ws: Workspace | None = None, str
     with _On(keys.device, stream) as on:
         wp, wb = on.ws(workspace_size(n, pairs=True), ws)
         _check(lib().gbs_sort_pairs_typed(C.c_void_p(keys.data_ptr()), C.c_void_p(vp), n, kt, wp, wb, on.s))
+    return keys, vals
+
+
+KEY64_TYPES = {"uint64": 0, "int64": 1, "float64": 2}
+
+
+def _key64_type(t, key_type):
+    torch = _torch()
+    if key_type is None:
+        key_type = {torch.uint64: "uint64", torch.int64: "int64", torch.float64: "float64"}.get(t.dtype)
+        if key_type is None:
+            raise GbsError("keys must be uint64, int64 or float64")
+    if key_type not in KEY64_TYPES:
+        raise GbsError(f"key_type must be one of {sorted(KEY64_TYPES)}")
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or not t.is_contiguous() or t.element_size() != 8:
+        raise GbsError("keys must be a contiguous CUDA tensor of 8-byte elements")
+    return KEY64_TYPES[key_type]
+
+
+def sort64_workspace_size(n: int, pairs: bool = False) -> int:
+    b = C.c_size_t()
+    _check(lib().gbs_sort64_workspace_size(n, int(pairs), C.byref(b)))
+    return b.value
+
+
+def sort_keys64(keys, key_type=None, ws: Workspace | None = None, stream=None):
+    """Sort a CUDA uint64 / int64 / float64 tensor in place by its numeric value (floats in
+    IEEE-754 totalOrder).  Two stable 32-bit GBS passes + a gather (gbs_sort_keys64)."""
+    kt = _key64_type(keys, key_type)
+    n = keys.numel()
+    with _On(keys.device, stream) as on:
+        wp, wb = on.ws(sort64_workspace_size(n), ws)
+        _check(lib().gbs_sort_keys64(C.c_void_p(keys.data_ptr()), n, kt, wp, wb, on.s))
+    return keys
+
+
+def sort_pairs64(keys, vals, key_type=None, ws: Workspace | None = None, stream=None):
+    """Stable sort of (64-bit key, 32-bit value) pairs by key, in place."""
+    kt = _key64_type(keys, key_type)
+    n = keys.numel()
+    if vals.numel() != n:
+        raise GbsError("keys and vals must have the same length")
+    vp = _dev_ptr(vals, "vals", keys.device)
+    with _On(keys.device, stream) as on:
+        wp, wb = on.ws(sort64_workspace_size(n, True), ws)
+        _check(lib().gbs_sort_pairs64(C.c_void_p(keys.data_ptr()), C.c_void_p(vp), n, kt, wp, wb, on.s))
     return keys, vals
 
 

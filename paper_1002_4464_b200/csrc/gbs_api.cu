@@ -1232,6 +1232,69 @@ gbs_status_t gbs_sort_pairs(uint32_t* d_keys, uint32_t* d_vals, size_t n, void* 
     return run_sort(d_keys, d_vals, n, nullptr, 0, d_ws, ws_bytes, (cudaStream_t)stream);
 }
 
+// 64-bit keys: LSD over the two 32-bit halves of the key's order-preserving image, each
+// pass a stable GBS of (half, index) pairs; then one gather of the original keys (and
+// values) by the final index permutation.  Workspace: the pairs sort's + lo/hi halves,
+// indices, a copy of the keys (and values).
+struct K64Layout {
+    size_t pairs_ws, half, idx, kcopy, vcopy, total;
+};
+static gbs_status_t k64_layout(size_t n, bool pairs, K64Layout* L)
+{
+    Plan P;
+    gbs_status_t r = make_plan(n, KIND_PAIRS, nullptr, P);
+    if (r) return r;
+    size_t o = 0;
+    auto al = [](size_t x) { return (x + 255) / 256 * 256; };
+    L->pairs_ws = o; o += al(P.ws);
+    L->half = o;     o += al(n * 4);
+    L->idx = o;      o += al(n * 4);
+    L->kcopy = o;    o += al(n * 8);
+    L->vcopy = o;    o += pairs ? al(n * 4) : 0;
+    L->total = o;
+    return GBS_SUCCESS;
+}
+
+static gbs_status_t run_sort64(void* keys, uint32_t* vals, size_t n, int type, void* ws, size_t ws_bytes, cudaStream_t st)
+{
+    if (type < GBS_KEY64_U64 || type > GBS_KEY64_F64) return fail(GBS_ERROR_INVALID_VALUE, "key_type %d", type);
+    K64Layout L;
+    gbs_status_t r = k64_layout(n, vals != nullptr, &L);
+    if (r) return r;
+    if (n <= 1) return GBS_SUCCESS;
+    if (!keys || ((uintptr_t)keys & 7)) return fail(GBS_ERROR_INVALID_VALUE, "d_keys NULL or not 8-byte aligned");
+    if (vals) {
+        if ((uintptr_t)vals & 3) return fail(GBS_ERROR_INVALID_VALUE, "d_vals not 4-byte aligned");
+        const uintptr_t k0 = (uintptr_t)keys, k1 = k0 + n * 8, v0 = (uintptr_t)vals, v1 = v0 + n * 4;
+        if (k0 < v1 && v0 < k1) return fail(GBS_ERROR_INVALID_VALUE, "keys and values overlap");
+    }
+    if (ws_bytes < L.total) return fail(GBS_ERROR_WORKSPACE_TOO_SMALL, "workspace %zu < %zu bytes", ws_bytes, L.total);
+    if (!ws || ((uintptr_t)ws & 255)) return fail(GBS_ERROR_INVALID_VALUE, "workspace NULL or not 256-byte aligned");
+    r = check_device();
+    if (r) return r;
+    char* w = reinterpret_cast<char*>(ws);
+    auto* k = reinterpret_cast<unsigned long long*>(keys);
+    uint32_t* half = reinterpret_cast<uint32_t*>(w + L.half);
+    uint32_t* idx = reinterpret_cast<uint32_t*>(w + L.idx);
+    auto* kc = reinterpret_cast<unsigned long long*>(w + L.kcopy);
+    uint32_t* vc = vals ? reinterpret_cast<uint32_t*>(w + L.vcopy) : nullptr;
+    const unsigned grid = num_sms() * 8;
+    launch_k(k_k64_lo, grid, 256, 0, st, (const unsigned long long*)k, (uint64_t)n, type, half, idx);
+    GBS_CUDA(cudaGetLastError());
+    r = run_sort(half, idx, n, nullptr, 0, w + L.pairs_ws, L.half - L.pairs_ws, st);    // pass 1: by the low half
+    if (r) return r;
+    launch_k(k_k64_hi, grid, 256, 0, st, (const unsigned long long*)k, (uint64_t)n, type, (const uint32_t*)idx, half);
+    GBS_CUDA(cudaGetLastError());
+    r = run_sort(half, idx, n, nullptr, 0, w + L.pairs_ws, L.half - L.pairs_ws, st);    // pass 2: by the high half
+    if (r) return r;
+    GBS_CUDA(cudaMemcpyAsync(kc, k, n * 8, cudaMemcpyDeviceToDevice, st));
+    if (vals) GBS_CUDA(cudaMemcpyAsync(vc, vals, n * 4, cudaMemcpyDeviceToDevice, st));
+    launch_k(k_k64_gather, grid, 256, 0, st, (const unsigned long long*)kc, (const uint32_t*)idx, (uint64_t)n, k,
+             (const uint32_t*)vc, vals);
+    GBS_CUDA(cudaGetLastError());
+    return GBS_SUCCESS;
+}
+
 // Typed keys: validate everything run_sort would (so nothing is enqueued on a bad call),
 // transform the keys in place, sort them as u32, transform back.
 static gbs_status_t run_sort_typed(void* keys, uint32_t* vals, size_t n, int type, void* ws, size_t ws_bytes,
@@ -1275,6 +1338,28 @@ gbs_status_t gbs_sort_pairs_typed(void* d_keys, uint32_t* d_vals, size_t n, int 
 {
     if (n > 1 && !d_vals) return fail(GBS_ERROR_INVALID_VALUE, "d_vals is NULL");
     return run_sort_typed(d_keys, d_vals, n, key_type, d_ws, ws_bytes, (cudaStream_t)stream);
+}
+
+gbs_status_t gbs_sort64_workspace_size(size_t n, int pairs, size_t* bytes)
+{
+    if (!bytes) return fail(GBS_ERROR_INVALID_VALUE, "bytes is NULL");
+    K64Layout L;
+    gbs_status_t r = k64_layout(n, pairs != 0, &L);
+    if (r) return r;
+    *bytes = L.total;
+    return GBS_SUCCESS;
+}
+
+gbs_status_t gbs_sort_keys64(void* d_keys, size_t n, int key_type, void* d_ws, size_t ws_bytes, gbs_stream_t stream)
+{
+    return run_sort64(d_keys, nullptr, n, key_type, d_ws, ws_bytes, (cudaStream_t)stream);
+}
+
+gbs_status_t gbs_sort_pairs64(void* d_keys, uint32_t* d_vals, size_t n, int key_type, void* d_ws, size_t ws_bytes,
+                              gbs_stream_t stream)
+{
+    if (n > 1 && !d_vals) return fail(GBS_ERROR_INVALID_VALUE, "d_vals is NULL");
+    return run_sort64(d_keys, d_vals, n, key_type, d_ws, ws_bytes, (cudaStream_t)stream);
 }
 
 gbs_status_t gbs_sort_ex(uint32_t* d_keys, uint32_t* d_vals, size_t n, const gbs_config_t* cfg, int stop_after_step,

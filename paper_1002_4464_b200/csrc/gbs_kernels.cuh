@@ -1499,6 +1499,44 @@ __global__ void k_key_transform(uint32_t* k, uint64_t n, int type, int inverse)
     for (uint64_t e = nv * 4 + tid; e < n; e += stride) k[e] = inverse ? key_inv(k[e], type) : key_fwd(k[e], type);
 }
 
+// 64-bit keys (gbs_sort_keys64 / gbs_sort_pairs64, NEXT-4): the sort key of a 64-bit
+// item is an order-preserving u64 image of its bits -- u64 as is, i64 with the sign bit
+// flipped, f64 in IEEE-754 totalOrder (negatives -> ~x, others -> x ^ 2^63) -- sorted as
+// the composite (hi, lo) of two u32 halves by two stable passes (lo, then hi).
+__device__ __forceinline__ unsigned long long key64_image(unsigned long long x, int type)
+{
+    if (type == 1) return x ^ (1ull << 63);
+    if (type == 2) return x ^ ((x >> 63) ? ~0ull : (1ull << 63));
+    return x;
+}
+// pass 1 input: lo[i] = low half of key i's image, idx[i] = i (the stable sort's values)
+__global__ void k_k64_lo(const unsigned long long* keys, uint64_t n, int type, uint32_t* lo, uint32_t* idx)
+{
+    pdl_entry();
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        lo[i] = (uint32_t)key64_image(keys[i], type);
+        idx[i] = (uint32_t)i;
+    }
+}
+// pass 2 input: hi[i] = high half of the image of the key pass 1 put at position i
+__global__ void k_k64_hi(const unsigned long long* keys, uint64_t n, int type, const uint32_t* idx, uint32_t* hi)
+{
+    pdl_entry();
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        hi[i] = (uint32_t)(key64_image(keys[idx[i]], type) >> 32);
+}
+// output: out[i] = in[idx[i]] (the original bits), values likewise
+__global__ void k_k64_gather(const unsigned long long* in, const uint32_t* idx, uint64_t n, unsigned long long* out,
+                             const uint32_t* vin, uint32_t* vout)
+{
+    pdl_entry();
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t j = idx[i];
+        out[i] = in[j];
+        if (vin) vout[i] = vin[j];
+    }
+}
+
 // Debug-only invariant checks (GBS_DEBUG_SYNC): *flag |= 1 if some problem's sorted
 // samples are out of order, |= 2 if some row of a does not sum to the sublist's
 // real item count (conservation).

@@ -265,3 +265,30 @@ def test_psrs_outer_level(p, dist):
     assert counts.sum() == k.size
     assert counts.max() <= n_local + (p - 1) * (n_local // s_r - 1)
     assert np.all(np.diff(cuts, axis=1) >= 0) and np.all(cuts[:, -1] == n_local)
+
+
+# --- 64-bit keys: the oracle's plain definition, pinned ----------------------------------
+
+def test_sort64_pins():
+    """oracle.sort64 against hand values (IEEE-754 totalOrder, section 5.10) and numpy."""
+    f = np.array([1.0, -0.0, 0.0, -np.inf, np.inf, -1.0, 0.0, -0.0], np.float64)
+    nan_pos = np.array([0x7FF8000000000001], np.uint64).view(np.float64)[0]
+    nan_neg = np.array([0xFFF8000000000001], np.uint64).view(np.float64)[0]
+    x = np.concatenate([f, [nan_pos, nan_neg]])
+    vals = np.arange(x.size, dtype=np.uint32)
+    k, v = oracle.sort64(x, vals, "float64")
+    # -NaN, -inf, -1, -0 (input 1), -0 (input 7), +0 (2), +0 (6), 1, inf, +NaN
+    assert list(v) == [9, 3, 5, 1, 7, 2, 6, 0, 4, 8]
+    rng = np.random.default_rng(0)
+    u = rng.integers(0, 1 << 63, 5000, dtype=np.uint64) * 2 + rng.integers(0, 2, 5000, dtype=np.uint64)
+    u[::7] = u[0]
+    ks, vs = oracle.sort64(u, np.arange(u.size, dtype=np.uint32), "uint64")
+    order = np.argsort(u, kind="stable")
+    assert np.array_equal(ks, u[order]) and np.array_equal(vs, order.astype(np.uint32))
+    i = u.view(np.int64)
+    ks, vs = oracle.sort64(i, np.arange(i.size, dtype=np.uint32), "int64")
+    order = np.argsort(i, kind="stable")
+    assert np.array_equal(ks, i[order]) and np.array_equal(vs, order.astype(np.uint32))
+    g = rng.standard_normal(3000) * 1e300
+    ks, _ = oracle.sort64(g, None, "float64")
+    assert np.array_equal(ks, np.sort(g))

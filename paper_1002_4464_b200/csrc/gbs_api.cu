@@ -90,6 +90,9 @@ constexpr uint32_t SMALL_TILE = 2048;      // small CTA configuration
 #ifndef GBS_FUSE_89
 #define GBS_FUSE_89 1     // fused Step 8+9 for CTA-bucket levels
 #endif
+#ifndef GBS_FUSE_PAIRS
+#define GBS_FUSE_PAIRS 0  // ... for pairs as well (A/B)
+#endif
 #ifndef GBS_FUSE_MIN_D
 #define GBS_FUSE_MIN_D 32 // ... whose average run d = L/s is at least this many items
 #endif
@@ -344,7 +347,8 @@ static int build_node(Plan& P, int kind, uint32_t B, uint64_t N, uint32_t pad_ba
         // and the runs are long enough (d = L/s items on average) for the gathered reads
         // not to over-fetch: at d = 16 (64-byte runs) the scattered reads cost what the
         // relocation pass costs (measured); at d >= 32 and on small inputs the fused path wins
-        if (GBS_FUSE_89 && kind == KIND_KEYS && P.nodes[idx].m <= gather_max_m(kind) &&
+        if (GBS_FUSE_89 && (kind == KIND_KEYS || (kind == KIND_PAIRS && GBS_FUSE_PAIRS)) &&
+            P.nodes[idx].m <= gather_max_m(kind) &&
             P.nodes[idx].d >= GBS_FUSE_MIN_D) {
             P.nodes[idx].fuse89 = true;
         } else {
@@ -657,6 +661,8 @@ struct Bufs {
     // out-of-place sorts (keys): where Step 2 writes the sorted sublists (in stays
     // read-only); null = in place (in)
     void* srt = nullptr;
+    // typed keys: transform at the first level's loads / the last level's stores
+    int xf_in = 0, xf_out = 0;
 };
 
 template <int KIND>
@@ -817,6 +823,8 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
     lv.out_v = bf.out_v;
     lv.pf_stride = num_sms();
     lv.presorted = pr.presorted;
+    lv.xf_in = bf.xf_in;
+    lv.xf_out = (nd.leaf || nd.step9 < 0) ? bf.xf_out : 0;
     lv.seg_min = 0;
     lv.seg_max = 0xFFFFFFFFu;
     if (nd.leaf) {
@@ -985,7 +993,7 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
         GBS_CUDA(cudaStreamWaitEvent(st, ev, 0));          // the call completes on st
     } else if (nd.step9 < 0) {
         gbs_status_t r9;
-        if constexpr (KIND == KIND_KEYS)
+        if constexpr (KIND == KIND_KEYS || (KIND == KIND_PAIRS && GBS_FUSE_PAIRS))
             r9 = fuse ? launch_step9<KIND, MODE_GATHER>(lv, nd, ws, st) : launch_step9<KIND, MODE_BUCKET>(lv, nd, ws, st);
         else
             r9 = launch_step9<KIND, MODE_BUCKET>(lv, nd, ws, st);
@@ -999,6 +1007,7 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
         // the nested level sorts its problems in place in the reloc buffer and uses the
         // sublists' buffer (dead after Step 8) as its own relocation target
         Bufs b9{bf.reloc, bf.srt ? bf.srt : bf.in, bf.out, bf.reloc_v, bf.in_v, bf.out_v};
+        b9.xf_out = bf.xf_out;   // the keys entered the sort at this level's Step 2
         Probs p9{lv.child_off, lv.child_len, 0, 0};
         gbs_status_t r = exec(P, nd.step9, ws, b9, p9, st, 0);
         if (r) return r;
@@ -1022,7 +1031,7 @@ static gbs_status_t check_device()
 }
 
 static gbs_status_t run_sort(uint32_t* keys, uint32_t* vals, size_t n, const gbs_config_t* cfg, int stop,
-                             void* ws, size_t ws_bytes, cudaStream_t st)
+                             void* ws, size_t ws_bytes, cudaStream_t st, int xf = 0)
 {
     const int kind = vals ? KIND_PAIRS : KIND_KEYS;
     Plan P;
@@ -1045,6 +1054,7 @@ static gbs_status_t run_sort(uint32_t* keys, uint32_t* vals, size_t n, const gbs
     const Node& top = P.nodes[0];
     Bufs bf{keys, top.leaf ? (void*)keys : (void*)(w + top.o_reloc), keys, vals,
             (top.leaf || !vals) ? vals : reinterpret_cast<uint32_t*>(w + top.o_reloc_v), vals};
+    bf.xf_in = bf.xf_out = xf;
     Probs pr{nullptr, nullptr, 0, (uint32_t)n};
     return exec(P, 0, w, bf, pr, st, stop);
 }
@@ -1317,14 +1327,8 @@ static gbs_status_t run_sort_typed(void* keys, uint32_t* vals, size_t n, int typ
     if (P.ws && (!ws || ((uintptr_t)ws & 255))) return fail(GBS_ERROR_INVALID_VALUE, "workspace NULL or not 256-byte aligned");
     r = check_device();
     if (r) return r;
-    const unsigned grid = num_sms() * 4;
-    launch_k(k_key_transform, grid, 256, 0, st, k, (uint64_t)n, type, 0);
-    GBS_CUDA(cudaGetLastError());
-    r = run_sort(k, vals, n, nullptr, 0, ws, ws_bytes, st);
-    if (r) return r;
-    launch_k(k_key_transform, grid, 256, 0, st, k, (uint64_t)n, type, 1);
-    GBS_CUDA(cudaGetLastError());
-    return GBS_SUCCESS;
+    // the transform runs inside the sort: at Step 2's load and the last Step 9's store
+    return run_sort(k, vals, n, nullptr, 0, ws, ws_bytes, st, type);
 }
 
 gbs_status_t gbs_sort_keys_typed(void* d_keys, size_t n, int key_type, void* d_ws, size_t ws_bytes,

@@ -89,6 +89,9 @@ struct LevelDev {
     // Step 7 records the longest run max a_ij here (zeroed with the look-back words);
     // Step 8 picks the grouped relocation only when runs are short (R21)
     uint32_t* maxrun;
+    // typed keys: the transform applied where keys enter (Step 2 / leaf loads from `in`)
+    // and leave (the last level's Step 9 / leaf stores to `out`); 0 = none
+    int xf_in, xf_out;
 };
 
 // L2 prefetch of a byte range (cp.async.bulk.prefetch: a TMA bulk operation, no
@@ -172,6 +175,24 @@ __device__ __forceinline__ unsigned long long pad64(uint32_t pad_base, uint64_t 
     return (0xFFFFFFFFull << 32) | (unsigned long long)(pad_base + (uint32_t)p_minus_N);
 }
 
+// Typed keys (NEXT-4): an order-preserving bijection of int32 / binary32 bit patterns onto
+// u32 (xf = 1: int32, x ^ 2^31; xf = 2: float, negatives -> ~x, others -> x ^ 2^31) and its
+// inverse.  Applied where keys enter the sort (Step 2's load, a leaf's load) and where they
+// leave it (the last level's Step 9 store, a leaf's store): every intermediate array is in
+// the u32 image, and no extra pass touches the keys (xf = 0: plain u32 keys).
+__device__ __forceinline__ uint32_t key_fwd(uint32_t x, int type)
+{
+    if (type == 1) return x ^ 0x80000000u;
+    return x ^ ((x >> 31) ? 0xFFFFFFFFu : 0x80000000u);
+}
+__device__ __forceinline__ uint32_t key_inv(uint32_t x, int type)
+{
+    if (type == 1) return x ^ 0x80000000u;
+    return x ^ ((x >> 31) ? 0x80000000u : 0xFFFFFFFFu);
+}
+__device__ __forceinline__ uint32_t xf_in(uint32_t x, int xf) { return xf ? key_fwd(x, xf) : x; }
+__device__ __forceinline__ uint32_t xf_out(uint32_t x, int xf) { return xf ? key_inv(x, xf) : x; }
+
 // ------------------------------------------------------------------ segment I/O
 // One tile of `v` items at element offset `off` of an HBM buffer: registers <- HBM
 // (load_regs), on-chip sort (CS::sort, result in shared memory), HBM <- shared memory
@@ -193,19 +214,24 @@ struct Seg {
 
     template <int M>
     static __device__ __forceinline__ void load_regs(T (&x)[M], const void* src, const uint32_t* src_v,
-                                                     uint64_t off, int v, unsigned char* smem)
+                                                     uint64_t off, int v, unsigned char* smem, int xf = 0)
     {
         if constexpr (KIND == KIND_PAIRS) {
             const int p0 = CS::load_pos(0), rem = v - p0;
             const uint32_t* s = reinterpret_cast<const uint32_t*>(src) + off + p0;
 #pragma unroll
             for (int k = 0; k < ITEMS; ++k) {
-                const uint32_t key = 32 * k < rem ? __ldg(s + 32 * k) : 0xFFFFFFFFu;
+                const uint32_t key = 32 * k < rem ? xf_in(__ldg(s + 32 * k), xf) : 0xFFFFFFFFu;
                 x[k] = ((T)key << 32) | (T)(uint32_t)(p0 + 32 * k);     // stable: ties by position
             }
             uint32_t* vsm = vsm_of(smem);
             const uint32_t* sv = src_v + off;
             for (int p = threadIdx.x; p < v; p += BLOCK) vsm[p] = __ldg(sv + p);
+        } else if constexpr (KIND == KIND_KEYS) {
+            const uint32_t* s = reinterpret_cast<const uint32_t*>(src) + off;
+            const int p0 = CS::load_pos(0), rem = v - p0;     // load_pos(k) = p0 + 32k
+#pragma unroll
+            for (int k = 0; k < ITEMS; ++k) x[k] = 32 * k < rem ? xf_in(s[p0 + 32 * k], xf) : CS::TMAX;
         } else {
             CS::load(x, reinterpret_cast<const KeyT*>(src) + off, v);
         }
@@ -259,7 +285,7 @@ struct Seg {
     }
 
     static __device__ __forceinline__ void store(void* dst, uint32_t* dst_v, uint64_t dst_off, int v,
-                                                 unsigned char* smem)
+                                                 unsigned char* smem, int xf = 0)
     {
         const T* sm = reinterpret_cast<const T*>(smem);
         if constexpr (KIND == KIND_KEYS) {
@@ -272,9 +298,9 @@ struct Seg {
                 uint32_t* d0 = d + t;
 #pragma unroll
                 for (int k = 0; k < ITEMS; ++k)
-                    if (t + k * BLOCK < v) d0[k * BLOCK] = (uint32_t)s0[k * (BLOCK + (BLOCK >> CS::PAD))];
+                    if (t + k * BLOCK < v) d0[k * BLOCK] = xf_out((uint32_t)s0[k * (BLOCK + (BLOCK >> CS::PAD))], xf);
             } else {
-                for (int p = threadIdx.x; p < v; p += BLOCK) d[p] = (uint32_t)sm[CS::phys(p)];
+                for (int p = threadIdx.x; p < v; p += BLOCK) d[p] = xf_out((uint32_t)sm[CS::phys(p)], xf);
             }
         } else if constexpr (KIND == KIND_PAIRS) {
             const uint32_t* vsm = vsm_of(smem);
@@ -282,7 +308,7 @@ struct Seg {
             uint32_t* dv = dst_v + dst_off;
             for (int p = threadIdx.x; p < v; p += BLOCK) {
                 const T c = sm[CS::phys(p)];
-                d[p] = (uint32_t)(c >> 32);
+                d[p] = xf_out((uint32_t)(c >> 32), xf);
                 dv[p] = vsm[(uint32_t)c];
             }
         } else {
@@ -321,12 +347,12 @@ struct Adapt {
 
     template <int M>
     static __device__ __forceinline__ void load(T (&x)[M], const void* src, const uint32_t* src_v, uint64_t off,
-                                                int v, unsigned char* smem)
+                                                int v, unsigned char* smem, int xf = 0)
     {
         if constexpr (HALF) {
-            if (v <= S::TILE / 2) { Sub::load(x, src, src_v, off, v, smem); return; }
+            if (v <= S::TILE / 2) { Sub::load(x, src, src_v, off, v, smem, xf); return; }
         }
-        S::load_regs(x, src, src_v, off, v, smem);
+        S::load_regs(x, src, src_v, off, v, smem, xf);
     }
     template <int M>
     static __device__ __forceinline__ void sort(T (&x)[M], unsigned char* smem, int v)
@@ -336,37 +362,39 @@ struct Adapt {
         }
         S::CS::sort(x, reinterpret_cast<T*>(smem), v);
     }
-    static __device__ __forceinline__ void store(void* dst, uint32_t* dst_v, uint64_t off, int v, unsigned char* smem)
+    static __device__ __forceinline__ void store(void* dst, uint32_t* dst_v, uint64_t off, int v, unsigned char* smem,
+                                                 int xf = 0)
     {
         if constexpr (HALF) {
-            if (v <= S::TILE / 2) { Sub::store(dst, dst_v, off, v, smem); return; }
+            if (v <= S::TILE / 2) { Sub::store(dst, dst_v, off, v, smem, xf); return; }
         }
-        S::store(dst, dst_v, off, v, smem);
+        S::store(dst, dst_v, off, v, smem, xf);
     }
     // fused Step 8+9: gather + sort + store, register array sized for the chosen tile
     template <typename G>
     static __device__ __forceinline__ void run_gather(const G& g, int v, void* dst, uint32_t* dst_v, uint64_t off,
-                                                      unsigned char* smem)
+                                                      unsigned char* smem, int xf_o = 0)
     {
         if constexpr (HALF) {
-            if (v <= S::TILE / 2) { Sub::run_gather(g, v, dst, dst_v, off, smem); return; }
+            if (v <= S::TILE / 2) { Sub::run_gather(g, v, dst, dst_v, off, smem, xf_o); return; }
         }
         T x[ITEMS];
         S::load_gather(x, g, v, smem);
         S::CS::sort(x, reinterpret_cast<T*>(smem), v);
-        S::store(dst, dst_v, off, v, smem);
+        S::store(dst, dst_v, off, v, smem, xf_o);
     }
     // load + sort + store with a register array sized for the chosen tile
     static __device__ __forceinline__ void run(const void* src, const uint32_t* src_v, uint64_t off, int v,
-                                               void* dst, uint32_t* dst_v, unsigned char* smem)
+                                               void* dst, uint32_t* dst_v, unsigned char* smem, int xf_i = 0,
+                                               int xf_o = 0)
     {
         if constexpr (HALF) {
-            if (v <= S::TILE / 2) { Sub::run(src, src_v, off, v, dst, dst_v, smem); return; }
+            if (v <= S::TILE / 2) { Sub::run(src, src_v, off, v, dst, dst_v, smem, xf_i, xf_o); return; }
         }
         T x[ITEMS];
-        S::load_regs(x, src, src_v, off, v, smem);
+        S::load_regs(x, src, src_v, off, v, smem, xf_i);
         S::CS::sort(x, reinterpret_cast<T*>(smem), v);
-        S::store(dst, dst_v, off, v, smem);
+        S::store(dst, dst_v, off, v, smem, xf_o);
     }
 };
 
@@ -397,7 +425,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_local_sort(LevelDev lv)
     int v = 0;
     if (tile < ntiles) {
         sublist_of(lv, tile, start, v);
-        if (pipe) S::load_regs(x, lv.in, lv.in_v, start, v, smem_raw);
+        if (pipe) S::load_regs(x, lv.in, lv.in_v, start, v, smem_raw, lv.xf_in);
     }
     for (; tile < ntiles; tile += gridDim.x) {
         const uint32_t b = tile / lv.m, i = tile % lv.m;
@@ -419,11 +447,11 @@ __global__ void __launch_bounds__(BLOCK, 1) k_local_sort(LevelDev lv)
                     S::CS::sort_presorted(x, reinterpret_cast<const unsigned long long*>(lv.in) + start, sm, v,
                                           (int)lv.presorted);
             } else {
-                if (!pipe) S::load_regs(x, lv.in, lv.in_v, start, v, smem_raw);
+                if (!pipe) S::load_regs(x, lv.in, lv.in_v, start, v, smem_raw, lv.xf_in);
                 S::CS::sort(x, sm, v);
             }
         }
-        if (pipe && nv > 0) S::load_regs(x, lv.in, lv.in_v, nstart, nv, smem_raw);   // in flight during the store
+        if (pipe && nv > 0) S::load_regs(x, lv.in, lv.in_v, nstart, nv, smem_raw, lv.xf_in);   // in flight during the store
         if (v > 0) S::store(lv.srt, lv.srt_v, start, v, smem_raw);
         u64* smp = lv.samples + ((uint64_t)b * lv.m + i) * lv.s;
         for (uint32_t k = threadIdx.x; k < lv.s; k += BLOCK) {
@@ -486,7 +514,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BLOCK, 1) k_local_so
             const int nr = max(0, min(nv - rank * H, H));
             if (nr > 0) prefetch_l2(reinterpret_cast<const T*>(lv.in) + ns + (uint64_t)rank * H, (size_t)nr * 4);
         }
-        S::load_regs(x, lv.in, nullptr, start + (uint64_t)rank * H, vr, smem_raw);
+        S::load_regs(x, lv.in, nullptr, start + (uint64_t)rank * H, vr, smem_raw, lv.xf_in);
         CS::sort(x, sm, vr);                            // positions >= vr read as TMAX
         cluster.sync();                                 // both halves sorted and visible
         const T* peer = cluster.map_shared_rank(sm, rank ^ 1);
@@ -1407,7 +1435,7 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK <= 576 ? 2 : 1)) k_segment_sort(
         const uint64_t pb = lv.pr.offset(b);
         GatherSrc g{reinterpret_cast<const KeyT*>(lv.srt) + pb, KIND == KIND_PAIRS ? lv.srt_v + pb : nullptr, run,
                     (int)lv.m};
-        A::run_gather(g, v, lv.out, lv.out_v, off, smem_raw);
+        A::run_gather(g, v, lv.out, lv.out_v, off, smem_raw, lv.xf_out);
         return;
     }
     const void* src = MODE == MODE_LEAF ? lv.in : lv.reloc;
@@ -1428,7 +1456,7 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK <= 576 ? 2 : 1)) k_segment_sort(
         uint64_t off;
         int v;
         segment_of<MODE>(lv, lv.tier_list[blockIdx.x], off, v);
-        A::run(src, src_v, off, v, lv.out, lv.out_v, smem_raw);
+        A::run(src, src_v, off, v, lv.out, lv.out_v, smem_raw, MODE == MODE_LEAF ? lv.xf_in : 0, lv.xf_out);
         return;
     }
     const uint32_t count = MODE == MODE_LEAF ? lv.B : lv.B * lv.s;
@@ -1446,7 +1474,7 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK <= 576 ? 2 : 1)) k_segment_sort(
     int v;
     segment_of<MODE>(lv, lv.seg_lo + blockIdx.x, off, v);
     if (v <= 0 || (uint32_t)v <= lv.seg_min || (uint32_t)v > lv.seg_max) return;
-    A::run(src, src_v, off, v, lv.out, lv.out_v, smem_raw);
+    A::run(src, src_v, off, v, lv.out, lv.out_v, smem_raw, MODE == MODE_LEAF ? lv.xf_in : 0, lv.xf_out);
 }
 
 // The full-tile size tier of Step 9 (buckets above 5/8 of a tile: rare, none for
@@ -1465,38 +1493,8 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK <= 576 ? 2 : 1)) k_segment_sort_
         uint64_t off;
         int v;
         segment_of<MODE_BUCKET>(lv, lv.tier_list[q], off, v);
-        A::run(lv.reloc, lv.reloc_v, off, v, lv.out, lv.out_v, smem_raw);
+        A::run(lv.reloc, lv.reloc_v, off, v, lv.out, lv.out_v, smem_raw, 0, lv.xf_out);
     }
-}
-
-// Typed keys (gbs_sort_keys_typed, NEXT-4): an order-preserving bijection of int32 /
-// binary32 bit patterns onto u32, in place (inverse = 1 undoes it).  int32: x ^ 2^31.
-// float: negatives (sign set) -> ~x, others -> x ^ 2^31; inverse: top bit set -> x ^ 2^31,
-// else ~x.  16-byte vectors when the buffer is 16-byte aligned.
-__device__ __forceinline__ uint32_t key_fwd(uint32_t x, int type)
-{
-    if (type == 1) return x ^ 0x80000000u;
-    return x ^ ((x >> 31) ? 0xFFFFFFFFu : 0x80000000u);
-}
-__device__ __forceinline__ uint32_t key_inv(uint32_t x, int type)
-{
-    if (type == 1) return x ^ 0x80000000u;
-    return x ^ ((x >> 31) ? 0x80000000u : 0xFFFFFFFFu);
-}
-__global__ void k_key_transform(uint32_t* k, uint64_t n, int type, int inverse)
-{
-    pdl_entry();
-    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (uint64_t)gridDim.x * blockDim.x;
-    const bool vec = ((uintptr_t)k & 15) == 0;
-    const uint64_t nv = vec ? n / 4 : 0;
-    uint4* k4 = reinterpret_cast<uint4*>(k);
-    for (uint64_t q = tid; q < nv; q += stride) {
-        uint4 v = k4[q];
-        if (inverse) { v.x = key_inv(v.x, type); v.y = key_inv(v.y, type); v.z = key_inv(v.z, type); v.w = key_inv(v.w, type); }
-        else { v.x = key_fwd(v.x, type); v.y = key_fwd(v.y, type); v.z = key_fwd(v.z, type); v.w = key_fwd(v.w, type); }
-        k4[q] = v;
-    }
-    for (uint64_t e = nv * 4 + tid; e < n; e += stride) k[e] = inverse ? key_inv(k[e], type) : key_fwd(k[e], type);
 }
 
 // 64-bit keys (gbs_sort_keys64 / gbs_sort_pairs64, NEXT-4): the sort key of a 64-bit

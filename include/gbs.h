@@ -66,9 +66,10 @@ gbs_status_t gbs_sort_pairs(uint32_t* d_keys, uint32_t* d_vals, size_t n, void* 
                             size_t ws_bytes, gbs_stream_t stream);
 
 /* Key types beyond unsigned 32-bit (the paper never fixes the item
- * type, R1).  Signed int32 and IEEE-754 binary32 keys are sorted as u32 keys after
- * an order-preserving bijection of their bits, applied in place before the sort and
- * inverted after it (two streaming kernels, both on `stream`):
+ * type, R1).  Signed int32 and IEEE-754 binary32 keys are sorted as u32 keys under
+ * an order-preserving bijection of their bits, applied where the keys enter the sort
+ * (Step 2's load) and inverted where they leave it (the last Step 9's store), so no pass
+ * is added:
  *   GBS_KEY_I32: flip the sign bit;
  *   GBS_KEY_F32: negative (sign set) -> flip every bit, otherwise flip the sign bit.
  * Float order is the IEEE-754 totalOrder of the bit patterns: -NaN < -inf < ... < -0 <

@@ -1306,7 +1306,8 @@ static gbs_status_t run_sort64(void* keys, uint32_t* vals, size_t n, int type, v
 }
 
 // Typed keys: validate everything run_sort would (so nothing is enqueued on a bad call),
-// transform the keys in place, sort them as u32, transform back.
+// then sort the keys' u32 images: the transform is applied where keys enter the sort
+// (Step 2's load) and inverted where they leave it (the last level's Step 9 store).
 static gbs_status_t run_sort_typed(void* keys, uint32_t* vals, size_t n, int type, void* ws, size_t ws_bytes,
                                    cudaStream_t st)
 {

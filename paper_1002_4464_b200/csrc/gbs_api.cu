@@ -90,6 +90,9 @@ constexpr uint32_t SMALL_TILE = 2048;      // small CTA configuration
 #ifndef GBS_FUSE_89
 #define GBS_FUSE_89 1     // fused Step 8+9 for CTA-bucket levels
 #endif
+#ifndef GBS_PAIR_BUCKETS
+#define GBS_PAIR_BUCKETS 1  // keys: Step 9 on CTA pairs when one-tile buckets would nest
+#endif
 #ifndef GBS_FUSE_PAIRS
 #define GBS_FUSE_PAIRS 0  // ... for pairs as well (A/B)
 #endif
@@ -132,6 +135,7 @@ struct Node {
     uint32_t pad_base = 0;
     bool local_small = false, bucket_small = false;
     bool local_pair = false;   // Step 2 on CTA pairs (L = 2 tiles, keys)
+    bool bucket_pair = false;  // Step 9 on CTA pairs (buckets up to 2 tiles, keys)
     int step4 = -1, step9 = -1;
     size_t o_samples = 0, o_splitters = 0, o_a = 0, o_l = 0, o_state = 0;
     size_t o_child_off = 0, o_child_len = 0, o_reloc = SIZE_MAX, o_reloc_v = SIZE_MAX;
@@ -294,6 +298,15 @@ static int build_node(Plan& P, int kind, uint32_t B, uint64_t N, uint32_t pad_ba
                 for (uint32_t c = 2; c <= 2 * tile / D_MIN; c *= 2)
                     if (hi_bound(N, 2 * tile, c) <= tile) { L = 2 * tile; s = c; break; }
             }
+            // keys with no one-level plan at one-tile buckets: buckets of two tiles sorted
+            // by CTA pairs (NEXT-2, R20) when that gives one level (2^27: 2^16-key sublists,
+            // s = 4096, bound 63,473) -- one fewer CTA-sort pass than a nested Step 9
+            if (kind == KIND_KEYS && B == 1 && !s && GBS_PAIR_BUCKETS) {
+                for (uint32_t Lc = 2 * tile; Lc >= tile && !s; Lc /= 2)
+                    for (uint32_t c = 2; c <= Lc / D_MIN && c <= MAX_S; c *= 2)
+                        if (hi_bound(N, Lc, c) <= 2 * tile) { L = Lc; s = c; break; }
+                if (s) nd.bucket_pair = true;
+            }
             if (!s) s = L / D_NEST;
         }
     }
@@ -335,7 +348,9 @@ static int build_node(Plan& P, int kind, uint32_t B, uint64_t N, uint32_t pad_ba
         if (c4 < 0) return -1;
         P.nodes[idx].step4 = c4;
     }
-    if (nd.hi <= tile) {
+    if (nd.bucket_pair) {
+        P.launches += 1 + reloc_launches(kind);   // relocate + the CTA-pair bucket sort
+    } else if (nd.hi <= tile) {
         P.nodes[idx].bucket_small = nd.hi <= SMALL_TILE;
         // buckets that may exceed half a tile: size tiers (see exec_kind)
         P.launches += step9_launches(kind, P.nodes[idx]);
@@ -509,6 +524,20 @@ static void launch_local_pair(const LevelDev& lv, cudaStream_t st)
     });
     const unsigned pairs = std::min<unsigned>(lv.B * lv.m, num_sms() / 2);
     launch_k(k_local_sort_pair<BLOCK, ITEMS>, 2 * pairs, BLOCK, sm, st, lv);
+}
+
+// Step 9 on CTA pairs: one cluster of two per bucket slot, persistent (one CTA per SM)
+static void launch_seg_pair(const LevelDev& lv, unsigned count, cudaStream_t st)
+{
+    constexpr int BLOCK = GBS_KEYS_BLOCK, ITEMS = GBS_KEYS_ITEMS;
+    const size_t sm = Seg<KIND_KEYS, BLOCK, ITEMS>::smem_bytes();
+    static DevOnce once;
+    once.run([&] {
+        set_smem(k_segment_sort_pair<BLOCK, ITEMS>, sm);
+        return 1;
+    });
+    const unsigned pairs = std::min<unsigned>(count, num_sms() / 2);
+    launch_k(k_segment_sort_pair<BLOCK, ITEMS>, 2 * pairs, BLOCK, sm, st, lv);
 }
 
 template <int KIND>
@@ -974,7 +1003,11 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
             LevelDev lg = lv;
             lg.seg_lo = j0;
             lg.seg_hi = j1;
-            launch_seg<KIND, MODE_BUCKET>(lg, nd.bucket_small, j1 - j0, st);
+            if (nd.bucket_pair) {
+                if constexpr (KIND == KIND_KEYS) launch_seg_pair(lg, j1 - j0, st);
+            } else {
+                launch_seg<KIND, MODE_BUCKET>(lg, nd.bucket_small, j1 - j0, st);
+            }
             GBS_LAUNCHED();
             const uint64_t lo_cnt = (uint64_t)j1 * nd.m * nd.d;
             const uint64_t upto = j1 == nd.s ? hp->n : std::min<uint64_t>(hp->n, lo_cnt > V ? lo_cnt - V : 0);
@@ -991,6 +1024,9 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
         }
         GBS_CUDA(cudaEventRecord(ev, hp->cout));
         GBS_CUDA(cudaStreamWaitEvent(st, ev, 0));          // the call completes on st
+    } else if (nd.bucket_pair) {
+        if constexpr (KIND == KIND_KEYS) launch_seg_pair(lv, nd.B * nd.s, st);
+        GBS_LAUNCHED();
     } else if (nd.step9 < 0) {
         gbs_status_t r9;
         if constexpr (KIND == KIND_KEYS || (KIND == KIND_PAIRS && GBS_FUSE_PAIRS))

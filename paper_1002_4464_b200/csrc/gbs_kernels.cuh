@@ -1497,6 +1497,95 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK <= 576 ? 2 : 1)) k_segment_sort_
     }
 }
 
+// ------------------------------------------------------------ Step 9 on a CTA pair
+// SURVEY NEXT-2 for buckets: a bucket of up to 2 tiles (Step 9) sorted by a
+// cluster of two CTAs exactly as k_local_sort_pair sorts a two-tile sublist (each CTA
+// sorts half on chip, one merge-path split of the halves over DSMEM, swap, uneven local
+// merge), reading the relocated bucket and writing the final output.  Used when one-tile
+// buckets would need a nested level.  Keys only.
+template <int BLOCK, int ITEMS>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BLOCK, 1) k_segment_sort_pair(LevelDev lv)
+{
+    pdl_entry();
+    namespace cg = cooperative_groups;
+    using S = Seg<KIND_KEYS, BLOCK, ITEMS>;
+    using CS = typename S::CS;
+    using T = uint32_t;
+    constexpr int H = CS::TILE;                         // items per CTA (half a bucket)
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* sm = reinterpret_cast<T*>(smem_raw);
+    __shared__ int s_astar;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int rank = (int)cluster.block_rank();
+    const uint32_t count = lv.seg_hi ? lv.seg_hi : lv.B * lv.s;
+    const uint32_t ncl = gridDim.x / 2;
+    T x[ITEMS];
+    for (uint32_t q = lv.seg_lo + blockIdx.x / 2; q < count; q += ncl) {   // uniform in the pair
+        uint64_t off;
+        int v;
+        segment_of<MODE_BUCKET>(lv, q, off, v);
+        if (v <= 0) continue;                           // both CTAs skip
+        const int vr = max(0, min(v - rank * H, H));
+        if (threadIdx.x == 0 && q + ncl < count) {
+            uint64_t no;
+            int nv;
+            segment_of<MODE_BUCKET>(lv, q + ncl, no, nv);
+            const int nr = max(0, min(nv - rank * H, H));
+            if (nr > 0) prefetch_l2(reinterpret_cast<const T*>(lv.reloc) + no + (uint64_t)rank * H, (size_t)nr * 4);
+        }
+        S::load_regs(x, lv.reloc, nullptr, off + (uint64_t)rank * H, vr, smem_raw);
+        CS::sort(x, sm, vr);
+        cluster.sync();                                 // both halves sorted and visible
+        const T* peer = cluster.map_shared_rank(sm, rank ^ 1);
+        if (threadIdx.x < 32) {                         // a* = merge-path split of diagonal H
+            const T* A = rank == 0 ? sm : peer;
+            const T* B = rank == 0 ? peer : sm;
+            const int lane = threadIdx.x;
+            int lo = 0, hi = H;
+            while (lo < hi) {
+                const int step = (hi - lo + 31) / 32;
+                const int i = lo + lane * step;
+                const bool gt = i >= hi || A[CS::phys(i)] > B[CS::phys(H - 1 - i)];
+                const unsigned m = __ballot_sync(0xffffffffu, gt);
+                if (m == 0) {
+                    lo = lo + 31 * step + 1;
+                } else {
+                    const int f = __ffs(m) - 1;
+                    if (f == 0) hi = lo;
+                    else {
+                        hi = min(hi, lo + f * step);
+                        lo = lo + (f - 1) * step + 1;
+                    }
+                }
+            }
+            if (lane == 0) s_astar = lo;
+        }
+        __syncthreads();
+        const int astar = s_astar, bstar = H - astar;
+        static_assert(BLOCK % 32 == 0 && CS::PAD == 5, "swap addressing assumes one pad per 32");
+        constexpr int KSTEP = BLOCK + BLOCK / 32;
+        {
+            const int t = (int)threadIdx.x;
+            const T* src = peer + CS::phys((rank == 0 ? 0 : astar) + t);
+#pragma unroll
+            for (int k = 0; k < ITEMS; ++k) x[k] = t + k * BLOCK < bstar ? src[k * KSTEP] : T(0);
+            cluster.sync();                             // every remote read done
+            T* dst = sm + CS::phys((rank == 0 ? astar : 0) + t);
+#pragma unroll
+            for (int k = 0; k < ITEMS; ++k)
+                if (t + k * BLOCK < bstar) dst[k * KSTEP] = x[k];
+        }
+        __syncthreads();
+        CS::merge_two(x, sm, (int)threadIdx.x * ITEMS, rank == 0 ? astar : bstar);
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k) sm[CS::phys((int)threadIdx.x * ITEMS + k)] = x[k];
+        __syncthreads();
+        if (vr > 0) S::store(lv.out, nullptr, off + (uint64_t)rank * H, vr, smem_raw, lv.xf_out);
+        __syncthreads();                                // shared memory reused next bucket
+    }
+}
+
 // 64-bit keys (gbs_sort_keys64 / gbs_sort_pairs64, NEXT-4): the sort key of a 64-bit
 // item is an order-preserving u64 image of its bits -- u64 as is, i64 with the sign bit
 // flipped, f64 in IEEE-754 totalOrder (negatives -> ~x, others -> x ^ 2^63) -- sorted as

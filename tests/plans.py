@@ -15,6 +15,7 @@ D_NEST = 32             # d of a level whose buckets need a nested level
 PAIR_BELOW_D = 16       # keys: sublists of two tiles (CTA pairs) when the one-tile d is below
 SMALL_TILE = 1 << 11    # the small CTA configuration's tile (the paper's 2K sublists)
 SMALL_N_KEYS = 1 << 17  # keys problems up to this size: 2K sublists and buckets (latency: more CTAs)
+MAX_S = 4096            # samples per sublist Steps 6 and 8 hold in shared memory
 
 
 def hi_bound(cap: int, L: int, s: int) -> int:
@@ -58,6 +59,20 @@ def plan(n: int, tile: int = TILE_KEYS, cfg=None):
         if chosen is not None:
             levels.append((L, chosen))
             break
+        # keys, top level: buckets of two tiles (sorted by a CTA pair) when that gives
+        # one level -- sublists of two tiles first, then one tile
+        if tile == TILE_KEYS and not levels:
+            for Lc in (2 * tile, tile):
+                s = 2
+                while s <= Lc // D_MIN and s <= MAX_S and chosen is None:
+                    if hi_bound(cap, Lc, s) <= 2 * tile:
+                        L, chosen = Lc, s
+                    s *= 2
+                if chosen is not None:
+                    break
+            if chosen is not None:
+                levels.append((L, chosen))
+                break
         s = L // D_NEST
         levels.append((L, s))
         cap = hi_bound(cap, L, s)

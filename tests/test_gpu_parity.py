@@ -283,3 +283,43 @@ def test_nested_invariants_debug_mode(dev, args):
     r = subprocess.run([sys.executable, os.path.join(root, "scripts", "debug_nested.py"), *args],
                        capture_output=True, text=True, env=dict(os.environ, GBS_DEBUG_SYNC="1"), timeout=600)
     assert "ok equal: True" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("n,dist", [(1 << 27, "uniform"), (1 << 27, "zero"), (1 << 27, "staggered"),
+                                    ((1 << 27) + 12345, "det_duplicates"), (100_000_000, "gaussian")])
+def test_pair_buckets_one_level(dev, n, dist):
+    """Sizes whose one-tile buckets would need a nested Step 9 run one level with Step 9 on
+    CTA pairs (NEXT-2: buckets of up to 2^16 keys over DSMEM); == the plain definition."""
+    p = gbs.plan(n)
+    assert len(p["levels"]) == 1 and 1 << 15 < p["bucket_bound"][0] <= 1 << 16
+    keys = gi.generate_torch(dist, n, seed=2, device=dev)
+    ref = torch.sort(keys.to(torch.int64) & 0xFFFFFFFF).values
+    gbs.sort_keys(keys)
+    torch.cuda.synchronize()
+    assert torch.equal(keys.to(torch.int64) & 0xFFFFFFFF, ref)
+
+
+def test_pair_buckets_vs_oracle(dev):
+    """2^27 uniform keys, the pair-bucket plan [(65536, 4096)], against the CPU oracle run
+    with the same plan (element by element)."""
+    n = 1 << 27
+    keys = gi.generate("uniform", n, seed=9)
+    pl = plan(n)
+    assert pl == [(65536, 4096)]
+    exp, _, _ = oracle.gbs_sort(keys, plan=pl)
+    d = to_dev(keys, dev)
+    gbs.sort_keys(d)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_np(d), exp)
+
+
+def test_pair_buckets_host_pipeline(dev):
+    """gbs_sort_keys_host with the pair-bucket plan: chunked H2D + Step 2, bucket-group
+    D2H of the final prefix while later CTA-pair groups sort."""
+    n = (1 << 27) + 77
+    keys = gi.generate("bucket_sorted", n, seed=4)
+    h = torch.from_numpy(keys.view(np.int32).copy()).pin_memory()
+    d = torch.empty(n, dtype=torch.int32, device=dev)
+    gbs.sort_keys_host(h, d)
+    torch.cuda.synchronize()
+    assert np.array_equal(h.numpy().view(np.uint32), np.sort(keys))

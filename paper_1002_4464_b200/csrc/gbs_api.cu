@@ -94,7 +94,7 @@ constexpr uint32_t SMALL_TILE = 2048;      // small CTA configuration
 #define GBS_PAIR_BUCKETS 1  // keys: Step 9 on CTA pairs when one-tile buckets would nest
 #endif
 #ifndef GBS_FUSE_PAIRS
-#define GBS_FUSE_PAIRS 0  // ... for pairs as well (A/B)
+#define GBS_FUSE_PAIRS 1  // ... for pairs as well (C4: 81.6 -> 80.8 ms)
 #endif
 #ifndef GBS_FUSE_MIN_D
 #define GBS_FUSE_MIN_D 32 // ... whose average run d = L/s is at least this many items
@@ -349,7 +349,9 @@ static int build_node(Plan& P, int kind, uint32_t B, uint64_t N, uint32_t pad_ba
         P.nodes[idx].step4 = c4;
     }
     if (nd.bucket_pair) {
-        P.launches += 1 + reloc_launches(kind);   // relocate + the CTA-pair bucket sort
+        // relocate + tiers (k_bucket_tiers, <= C/2, <= C, CTA pairs)
+        P.launches += reloc_launches(kind) + 4;
+        P.nodes[idx].o_tiers = P.alloc(((uint64_t)B * s * 4 + 4) * 4);
     } else if (nd.hi <= tile) {
         P.nodes[idx].bucket_small = nd.hi <= SMALL_TILE;
         // buckets that may exceed half a tile: size tiers (see exec_kind)
@@ -833,6 +835,50 @@ static gbs_status_t launch_step9(const LevelDev& lv, const Node& nd, char* ws, c
     return GBS_SUCCESS;
 }
 
+// Step 9 of a level with two-tile buckets (keys): size tiers so a bucket takes the
+// smallest unit that holds it -- <= C/2 on 512-thread CTAs (2 per SM), <= C on one full
+// CTA, larger on a CTA pair (k_segment_sort_pair) -- all three concurrently (fork/join).
+// (One CTA pair per bucket measured 25.2 Gkeys/s at 2^27 against 26.8 for the nested
+// plan: the average bucket, n/s = C, half-fills a pair.)
+static gbs_status_t launch_step9_pair(const LevelDev& lv, const Node& nd, char* ws, cudaStream_t st)
+{
+    constexpr int KIND = KIND_KEYS;
+    const uint32_t count = nd.B * nd.s;
+    uint32_t* lists = reinterpret_cast<uint32_t*>(ws + nd.o_tiers);
+    uint32_t* lens = lists + 4 * (uint64_t)count;
+    GBS_CUDA(cudaMemsetAsync(lens, 0, 16, st));
+    launch_k(k_bucket_tiers, (count + 255) / 256, 256, 0, st, lv, lists, lens, TILE_KEYS / 2, TILE_KEYS, TILE_KEYS);
+    GBS_LAUNCHED();
+    LevelDev tl[4];
+    for (int q = 0; q < 4; ++q) {
+        tl[q] = lv;
+        tl[q].tier_list = lists + q * (uint64_t)count;
+        tl[q].tier_len = lens + q;
+    }
+    cudaStream_t ss = side_stream(), ss2 = side_stream(3);
+    cudaEvent_t fork = scratch_event(0), join = scratch_event(1), join2 = scratch_event(2);
+    if (ss && ss2 && fork && join && join2) {
+        GBS_CUDA(cudaEventRecord(fork, st));
+        GBS_CUDA(cudaStreamWaitEvent(ss, fork, 0));
+        GBS_CUDA(cudaStreamWaitEvent(ss2, fork, 0));
+    } else {
+        ss = ss2 = nullptr;
+    }
+    launch_seg_pair(tl[3], count, ss2 ? ss2 : st);
+    GBS_LAUNCHED();
+    launch_seg_t<KIND, GBS_BIG_KEYS, MODE_BUCKET>(tl[1], count, ss ? ss : st);
+    GBS_LAUNCHED();
+    launch_seg_t<KIND, 512, GBS_KEYS_ITEMS, MODE_BUCKET>(tl[0], count, st);
+    GBS_LAUNCHED();
+    if (ss) {
+        GBS_CUDA(cudaEventRecord(join, ss));
+        GBS_CUDA(cudaEventRecord(join2, ss2));
+        GBS_CUDA(cudaStreamWaitEvent(st, join, 0));
+        GBS_CUDA(cudaStreamWaitEvent(st, join2, 0));
+    }
+    return GBS_SUCCESS;
+}
+
 template <int KIND>
 static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, Probs pr, cudaStream_t st, int stop,
                               const HostPipe* hp)
@@ -1025,8 +1071,10 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
         GBS_CUDA(cudaEventRecord(ev, hp->cout));
         GBS_CUDA(cudaStreamWaitEvent(st, ev, 0));          // the call completes on st
     } else if (nd.bucket_pair) {
-        if constexpr (KIND == KIND_KEYS) launch_seg_pair(lv, nd.B * nd.s, st);
-        GBS_LAUNCHED();
+        if constexpr (KIND == KIND_KEYS) {
+            gbs_status_t r9 = launch_step9_pair(lv, nd, ws, st);
+            if (r9) return r9;
+        }
     } else if (nd.step9 < 0) {
         gbs_status_t r9;
         if constexpr (KIND == KIND_KEYS || (KIND == KIND_PAIRS && GBS_FUSE_PAIRS))

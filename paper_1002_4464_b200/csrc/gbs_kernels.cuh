@@ -1517,19 +1517,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BLOCK, 1) k_segment_
     __shared__ int s_astar;
     cg::cluster_group cluster = cg::this_cluster();
     const int rank = (int)cluster.block_rank();
-    const uint32_t count = lv.seg_hi ? lv.seg_hi : lv.B * lv.s;
+    // all buckets [seg_lo, seg_hi) of the level, or a size tier's list (k_bucket_tiers)
+    const uint32_t count = lv.tier_list ? *lv.tier_len : (lv.seg_hi ? lv.seg_hi : lv.B * lv.s);
+    const uint32_t q0 = lv.tier_list ? 0u : lv.seg_lo;
+    auto seg = [&](uint32_t q) { return lv.tier_list ? lv.tier_list[q] : q; };
     const uint32_t ncl = gridDim.x / 2;
     T x[ITEMS];
-    for (uint32_t q = lv.seg_lo + blockIdx.x / 2; q < count; q += ncl) {   // uniform in the pair
+    for (uint32_t q = q0 + blockIdx.x / 2; q < count; q += ncl) {   // uniform in the pair
         uint64_t off;
         int v;
-        segment_of<MODE_BUCKET>(lv, q, off, v);
+        segment_of<MODE_BUCKET>(lv, seg(q), off, v);
         if (v <= 0) continue;                           // both CTAs skip
         const int vr = max(0, min(v - rank * H, H));
         if (threadIdx.x == 0 && q + ncl < count) {
             uint64_t no;
             int nv;
-            segment_of<MODE_BUCKET>(lv, q + ncl, no, nv);
+            segment_of<MODE_BUCKET>(lv, seg(q + ncl), no, nv);
             const int nr = max(0, min(nv - rank * H, H));
             if (nr > 0) prefetch_l2(reinterpret_cast<const T*>(lv.reloc) + no + (uint64_t)rank * H, (size_t)nr * 4);
         }

@@ -206,6 +206,16 @@ gbs_status_t gbs_get_unique_id(uint8_t id[GBS_UNIQUE_ID_BYTES]);
  * sorted so far (~4.1 n_local + 8 p^2 s_r bytes). */
 gbs_status_t gbs_comm_init(gbs_comm_t* comm, const uint8_t id[GBS_UNIQUE_ID_BYTES], int nranks,
                            int rank);
+/* The same without NCCL: the communicator's one host-side collective -- exchanging the
+ * window's IPC handles (and agreeing that every peer mapped) -- goes through `allgather`,
+ * a caller-supplied blocking host allgather (each rank passes `bytes` at send, receives
+ * nranks * bytes in rank order at recv; returns 0 on success).  The exchange is then
+ * peer memory only (GBS_ERROR_UNSUPPORTED when a peer cannot be mapped).  This lets
+ * several processes share one GPU (NCCL refuses two ranks on one device): tests run the
+ * real multi-process path -- IPC windows, cross-process barriers, pushes -- on one B200. */
+typedef int (*gbs_host_allgather_fn)(const void* send, void* recv, size_t bytes, void* ctx);
+gbs_status_t gbs_comm_init_host(gbs_comm_t* comm, int nranks, int rank, gbs_host_allgather_fn allgather,
+                                void* ctx);
 /* Exchange transport: 0 = peer memory when every peer maps (default), 1 = NCCL.
  * Collective (every rank sets the same mode). */
 gbs_status_t gbs_comm_set_exchange(gbs_comm_t comm, int mode);

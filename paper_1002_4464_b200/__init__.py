@@ -88,6 +88,7 @@ def lib():
             "gbs_profile_begin": [],
             "gbs_profile_end": [C.POINTER(StepTimes)],
             "gbs_comm_set_exchange": [p, C.c_int],
+            "gbs_comm_init_host": [C.POINTER(p), C.c_int, C.c_int, p, p],
             "gbs_sort64_workspace_size": [sz, C.c_int, C.POINTER(sz)],
             "gbs_sort_keys64": [p, sz, C.c_int, p, sz, p],
             "gbs_sort_pairs64": [p, p, sz, C.c_int, p, sz, p],
@@ -424,14 +425,34 @@ def exchange_plan(cuts, rank: int):
     return dict(send_off=so, send_cnt=sc, recv_off=ro, recv_cnt=rc, n_out=int(n_out[0]))
 
 
+HOST_ALLGATHER = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
+
+
 class Comm:
     """libgbs communicator (NCCL + peer-mapped windows), bootstrapped over a
-    torch.distributed group: rank 0 creates the NCCL unique id, the group broadcasts it."""
+    torch.distributed group: rank 0 creates the NCCL unique id, the group broadcasts it.
+    bootstrap="host": no NCCL -- the window handles are exchanged with the group's own
+    all_gather (any backend, e.g. gloo), so several processes may share one GPU."""
 
-    def __init__(self, group=None, exchange: str = "p2p"):
+    def __init__(self, group=None, exchange: str = "p2p", bootstrap: str = "nccl"):
         import torch.distributed as dist
         self.rank = dist.get_rank(group)
         self.nranks = dist.get_world_size(group)
+        if bootstrap == "host":
+            def allgather(send, recv, nbytes, _ctx):
+                try:
+                    mine = C.string_at(send, nbytes)
+                    out = [None] * self.nranks
+                    dist.all_gather_object(out, mine, group=group)
+                    C.memmove(recv, b"".join(out), nbytes * self.nranks)
+                    return 0
+                except Exception:  # noqa: BLE001
+                    return 1
+            self._cb = HOST_ALLGATHER(allgather)             # kept alive with the communicator
+            h = C.c_void_p()
+            _check(lib().gbs_comm_init_host(C.byref(h), self.nranks, self.rank, C.cast(self._cb, C.c_void_p), None))
+            self.handle = h
+            return
         obj = [get_unique_id() if self.rank == 0 else None]
         dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0,
                                    group=group)

@@ -386,7 +386,9 @@ __global__ void __launch_bounds__(KM_BLOCK) k_kway_merge(const uint32_t* recv, c
 
 // ------------------------------------------------------------------ communicator
 struct gbs_comm {
-    ncclComm_t nc;
+    ncclComm_t nc = nullptr;        // null: bootstrapped through a host allgather (P2P only)
+    gbs_host_allgather_fn hag = nullptr;
+    void* hag_ctx = nullptr;
     int nranks, rank, device;
     int mode;                       // 0 auto (P2P when every peer maps), 1 NCCL
     // window (P2P path): own allocation, every rank's base, device copies of the per-array
@@ -433,10 +435,14 @@ gbs_status_t ensure_window(gbs_comm* c, size_t bytes, cudaStream_t st)
         if (cudaIpcGetMemHandle(&h, c->win) != cudaSuccess) ok = 0;
         const size_t hb = sizeof(cudaIpcMemHandle_t);
         std::vector<char> all((size_t)c->nranks * hb);
-        CUDA_OK(cudaMemcpy(c->scratch + (size_t)c->rank * hb, &h, hb, cudaMemcpyHostToDevice));
-        NCCL_OK(ncclAllGather(c->scratch + (size_t)c->rank * hb, c->scratch, hb, ncclChar, c->nc, st));
-        CUDA_OK(cudaStreamSynchronize(st));
-        CUDA_OK(cudaMemcpy(all.data(), c->scratch, all.size(), cudaMemcpyDeviceToHost));
+        if (c->hag) {
+            if (c->hag(&h, all.data(), hb, c->hag_ctx) != 0) return gbs::fail_msg(GBS_ERROR_NCCL, "host allgather failed");
+        } else {
+            CUDA_OK(cudaMemcpy(c->scratch + (size_t)c->rank * hb, &h, hb, cudaMemcpyHostToDevice));
+            NCCL_OK(ncclAllGather(c->scratch + (size_t)c->rank * hb, c->scratch, hb, ncclChar, c->nc, st));
+            CUDA_OK(cudaStreamSynchronize(st));
+            CUDA_OK(cudaMemcpy(all.data(), c->scratch, all.size(), cudaMemcpyDeviceToHost));
+        }
         for (int k = 0; k < c->nranks && ok; ++k) {
             if (k == c->rank) continue;
             cudaIpcMemHandle_t hk;
@@ -448,15 +454,23 @@ gbs_status_t ensure_window(gbs_comm* c, size_t bytes, cudaStream_t st)
         }
         cudaGetLastError();
         // every rank must agree on the path
-        int* d_ok = reinterpret_cast<int*>(c->scratch);
-        CUDA_OK(cudaMemcpy(d_ok, &ok, sizeof ok, cudaMemcpyHostToDevice));
-        NCCL_OK(ncclAllReduce(d_ok, d_ok, 1, ncclInt, ncclMin, c->nc, st));
-        CUDA_OK(cudaStreamSynchronize(st));
-        CUDA_OK(cudaMemcpy(&ok, d_ok, sizeof ok, cudaMemcpyDeviceToHost));
+        if (c->hag) {
+            std::vector<int> oks(c->nranks);
+            if (c->hag(&ok, oks.data(), sizeof ok, c->hag_ctx) != 0) return gbs::fail_msg(GBS_ERROR_NCCL, "host allgather failed");
+            for (int v : oks) ok = std::min(ok, v);
+        } else {
+            int* d_ok = reinterpret_cast<int*>(c->scratch);
+            CUDA_OK(cudaMemcpy(d_ok, &ok, sizeof ok, cudaMemcpyHostToDevice));
+            NCCL_OK(ncclAllReduce(d_ok, d_ok, 1, ncclInt, ncclMin, c->nc, st));
+            CUDA_OK(cudaStreamSynchronize(st));
+            CUDA_OK(cudaMemcpy(&ok, d_ok, sizeof ok, cudaMemcpyDeviceToHost));
+        }
     } else if (c->nranks > 1) {
         ok = 0;
     }
     c->p2p = ok != 0;
+    if (c->nranks > 1 && !c->p2p && !c->nc)
+        return gbs::fail_msg(GBS_ERROR_UNSUPPORTED, "peer windows could not be mapped and the communicator has no NCCL");
     return GBS_SUCCESS;
 }
 
@@ -602,9 +616,35 @@ gbs_status_t gbs_comm_init(gbs_comm_t* comm, const uint8_t id[GBS_UNIQUE_ID_BYTE
     return GBS_SUCCESS;
 }
 
+gbs_status_t gbs_comm_init_host(gbs_comm_t* comm, int nranks, int rank, gbs_host_allgather_fn allgather, void* ctx)
+{
+    if (!comm || !allgather || nranks < 1 || rank < 0 || rank >= nranks)
+        return gbs::fail_msg(GBS_ERROR_INVALID_VALUE, "gbs_comm_init_host: bad arguments");
+    if (nranks > MAX_RANKS) return gbs::fail_msg(GBS_ERROR_UNSUPPORTED, "gbs_comm_init_host: more than 16 ranks");
+    gbs_comm* c = new (std::nothrow) gbs_comm();
+    if (!c) return gbs::fail_msg(GBS_ERROR_INVALID_VALUE, "out of host memory");
+    c->nranks = nranks;
+    c->rank = rank;
+    c->mode = 0;
+    c->hag = allgather;
+    c->hag_ctx = ctx;
+    cudaGetDevice(&c->device);
+    if (cudaMallocHost(&c->h_cuts, 8) != cudaSuccess || cudaMalloc(&c->scratch, 64 * 1024) != cudaSuccess ||
+        cudaMalloc(&c->d_tab, 4 * MAX_RANKS * sizeof(void*)) != cudaSuccess) {
+        if (c->h_cuts) cudaFreeHost(c->h_cuts);
+        if (c->scratch) cudaFree(c->scratch);
+        delete c;
+        return gbs::fail_msg(GBS_ERROR_CUDA, "gbs_comm_init_host: allocation failed");
+    }
+    for (auto& e : c->ev) cudaEventCreate(&e);
+    *comm = c;
+    return GBS_SUCCESS;
+}
+
 gbs_status_t gbs_comm_set_exchange(gbs_comm_t comm, int mode)
 {
     if (!comm || mode < 0 || mode > 1) return gbs::fail_msg(GBS_ERROR_INVALID_VALUE, "gbs_comm_set_exchange: bad arguments");
+    if (mode == 1 && !comm->nc) return gbs::fail_msg(GBS_ERROR_UNSUPPORTED, "a host-bootstrapped communicator has no NCCL");
     if (comm->mode != mode) {
         cudaDeviceSynchronize();
         close_window(comm);
@@ -618,7 +658,7 @@ gbs_status_t gbs_comm_destroy(gbs_comm_t comm)
     if (!comm) return GBS_SUCCESS;
     cudaDeviceSynchronize();
     close_window(comm);
-    ncclResult_t r = ncclCommDestroy(comm->nc);
+    ncclResult_t r = comm->nc ? ncclCommDestroy(comm->nc) : ncclSuccess;
     cudaFreeHost(comm->h_cuts);
     cudaFree(comm->scratch);
     cudaFree(comm->d_tab);

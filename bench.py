@@ -67,6 +67,9 @@ def parse():
     ap.add_argument("--force-dist", action="store_true",
                     help="use the multi-GPU entry even with one rank (exercises E1-E9 on one GPU)")
     ap.add_argument("--lib", default=None, help="tuning only: load this libgbs build instead of the in-tree one")
+    ap.add_argument("--bootstrap", default="nccl", choices=["nccl", "host"],
+                    help="testing only (C5): 'host' = gloo group + host-bootstrapped communicator, so several "
+                         "ranks may share one GPU (exercises the multi-rank path on a one-GPU box)")
     ap.add_argument("--ncu-one", action="store_true",
                     help="profiling only: run exactly one sort of the workload (for ncu captures) and exit")
     a = ap.parse_args()
@@ -377,7 +380,10 @@ def main():
     if multi:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29531")
-        dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
+        if args.bootstrap == "host":
+            dist.init_process_group("gloo", rank=rank, world_size=world)
+        else:
+            dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
     if args.lib:
         gbs.LIB_PATH = args.lib
     elif rank == 0:
@@ -625,7 +631,9 @@ def run_c5(args, torch, dist, gi, gbs, dev, world, rank, local, stream, flush, p
     n = N // world
     pristine = gi.generate_torch(args.dist, N, seed=0, device=dev, start=n * rank, count=n)
     keys = pristine.clone()
-    comm = gbs.Comm()
+    comm = gbs.Comm(bootstrap=args.bootstrap)
+    # the group's collectives run on the device for NCCL, on the host for gloo
+    cdev = dev if args.bootstrap == "nccl" else torch.device("cpu")
     ws = gbs.Workspace(dev)
     _, cap = gbs.dist_workspace_size(n, world)
     out = torch.empty(cap, dtype=torch.int32, device=dev)
@@ -645,7 +653,7 @@ def run_c5(args, torch, dist, gi, gbs, dev, world, rank, local, stream, flush, p
     info = torch.stack([fin, fout, torch.tensor(part.numel(), device=dev),
                         p64[0] if part.numel() else torch.tensor(-1, device=dev),
                         p64[-1] if part.numel() else torch.tensor(-1, device=dev),
-                        torch.tensor(int(ok_sorted), device=dev)])
+                        torch.tensor(int(ok_sorted), device=dev)]).to(cdev)
     allinfo = [torch.empty_like(info) for _ in range(world)]
     dist.all_gather(allinfo, info)
     rows = [t.tolist() for t in allinfo]
@@ -679,7 +687,7 @@ def run_c5(args, torch, dist, gi, gbs, dev, world, rank, local, stream, flush, p
     torch.cuda.synchronize()
     ph = gbs.dist_profile_end()
     t = torch.tensor([statistics.mean(step_ms), ph.get("exchange_ms", 0.0), ph.get("exchange_bytes", 0.0)],
-                     dtype=torch.float64, device=dev)
+                     dtype=torch.float64, device=cdev)
     tmax = t.clone()
     dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
     ms = float(tmax[0].item())
@@ -699,7 +707,7 @@ def run_c5(args, torch, dist, gi, gbs, dev, world, rank, local, stream, flush, p
         if i:
             e_ms.append(a.elapsed_time(b))
         moved = part.numel()
-    te = torch.tensor([statistics.mean(e_ms)], dtype=torch.float64, device=dev)
+    te = torch.tensor([statistics.mean(e_ms)], dtype=torch.float64, device=cdev)
     dist.all_reduce(te, op=dist.ReduceOp.MAX)
     em = float(te[0].item())
     comm.close()
@@ -712,7 +720,9 @@ def run_c5(args, torch, dist, gi, gbs, dev, world, rank, local, stream, flush, p
            "checks": checks, "clocks": clk.summary(),
            "e2e": {"value": N / (em / 1e3), "unit": "keys/s", "h2d_bytes_per_step": 4 * N,
                    "d2h_bytes_per_step": 4 * N, "ms_per_step": em},
-           "gpu_launches": ph.get("launches_per_sort", 0) * args.steps,
+           # our kernels per sort: the local sort's plan, plus (p > 1) samples, E4 sample sort,
+           # fine cuts, push, merge and (peer-memory path) three barriers
+           "gpu_launches": (gbs.plan(n)["kernels_per_sort"] + (0 if world == 1 else (8 if ph.get("path", "").startswith("peer") else 4))) * args.steps,
            "exchange": {"ms_max_over_ranks": ex_ms, "bytes_rank0": ex_bytes,
                         "nvlink_GBps_rank0": (ex_bytes / (ex_ms / 1e3) / 1e9) if ex_ms > 0 else None,
                         "nvlink_peak_GBps_per_direction": 900.0, "path": ph.get("path")},

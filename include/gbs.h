@@ -242,7 +242,8 @@ gbs_status_t gbs_sort_keys_dist(gbs_comm_t comm, const uint32_t* d_in, size_t n_
  * and this call (which ends the profile, like gbs_profile_end): ms[0] E1 local sort,
  * ms[1] E2-E7 (samples, cuts and their exchange), ms[2] E8 exchange (incl. its barrier),
  * ms[3] E9 merge, ms[5] the whole call; exchange_bytes = keys bytes this rank sent to
- * other ranks; path 1 = peer memory, 2 = NCCL, 0 = one rank. */
+ * other ranks; path 1 = peer memory, 2 = NCCL, 0 = one rank, 3 = the emulation
+ * (gbs_sort_keys_dist_emulated; phases summed over its ranks). */
 typedef struct {
     float ms[6];
     double exchange_bytes;

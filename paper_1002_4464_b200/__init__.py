@@ -498,7 +498,8 @@ def dist_profile_end() -> dict:
     c = max(out.calls, 1)
     d = {nm: out.ms[i] / c for i, nm in enumerate(names) if nm != "_"}
     d.update(calls=out.calls, exchange_bytes=out.exchange_bytes / c,
-             path={0: "one rank", 1: "peer memory (NVLink stores)", 2: "nccl"}.get(out.path))
+             path={0: "one rank", 1: "peer memory (NVLink stores)", 2: "nccl",
+                   3: "emulated (all ranks on one GPU, phases summed over ranks)"}.get(out.path))
     return d
 
 

@@ -919,22 +919,43 @@ gbs_status_t gbs_sort_keys_dist_emulated(int p, const uint32_t* d_keys, size_t n
     }
     CUDA_OK(cudaMemcpyAsync(tab, h, sizeof h, cudaMemcpyHostToDevice, st));
     // the phases of all ranks in turn; stream order stands in for the device barriers
+    // (profiling: events between the phases, summed over the ranks)
+    const bool prof = gbs::profiling();
+    cudaEvent_t ev[5] = {};
+    if (prof)
+        for (auto& e : ev) CUDA_OK(cudaEventCreate(&e));
+    if (prof) cudaEventRecord(ev[0], st);
     for (int k = 0; k < p; ++k)
         if ((r = phase_local(c[k]))) return r;                                             // E1
+    if (prof) cudaEventRecord(ev[1], st);
     for (int k = 0; k < p; ++k)
         if ((r = phase_samples(c[k], reinterpret_cast<u64* const*>(tab + MAX_RANKS), p, (size_t)k * c[k].s_r))) return r;
     for (int k = 0; k < p; ++k)
         if ((r = phase_cuts(c[k], reinterpret_cast<u64* const*>(tab + 2 * MAX_RANKS), p, (size_t)k * c[k].nq))) return r;
+    if (prof) cudaEventRecord(ev[2], st);
     for (int k = 0; k < p; ++k)
         if ((r = phase_push(c[k], reinterpret_cast<uint32_t* const*>(tab + 3 * MAX_RANKS)))) return r;   // E8
+    if (prof) cudaEventRecord(ev[3], st);
     for (int k = 0; k < p; ++k)
         if ((r = phase_merge(c[k]))) return r;                                             // E9
+    if (prof) cudaEventRecord(ev[4], st);
     std::vector<u64> words((size_t)p * 4);
     for (int k = 0; k < p; ++k) CUDA_OK(cudaMemcpyAsync(&words[(size_t)k * 4], c[k].words, 32, cudaMemcpyDeviceToHost, st));
     CUDA_OK(cudaStreamSynchronize(st));
     for (int k = 0; k < p; ++k) {
         if (words[(size_t)k * 4] > out_capacity) return gbs::fail_msg(GBS_ERROR_CUDA, "receive count exceeds the bound");
         n_out[k] = words[(size_t)k * 4];
+    }
+    if (prof) {
+        float ms[4], tot = 0;
+        for (int k = 0; k < 4; ++k) cudaEventElapsedTime(&ms[k], ev[k], ev[k + 1]);
+        cudaEventElapsedTime(&tot, ev[0], ev[4]);
+        for (int k = 0; k < 4; ++k) g_dprof.ms[k] += ms[k];
+        g_dprof.ms[5] += tot;
+        for (int k = 0; k < p; ++k) g_dprof.sent += (double)words[(size_t)k * 4 + 1];
+        g_dprof.calls += 1;
+        g_dprof.path = 3;
+        for (auto e : ev) cudaEventDestroy(e);
     }
     return GBS_SUCCESS;
 }

@@ -63,7 +63,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-buffer leg (profiling runs only)")
     ap.add_argument("--no-extras", action="store_true", help="skip the c2/c3/c5_base legs (profiling runs only)")
-    ap.add_argument("--n", type=int, default=0, help="override the workload's size (experiments; not a bench line)")
+    ap.add_argument("--size", type=int, default=0, help="override the workload's size (experiments; not a bench line)")
     ap.add_argument("--force-dist", action="store_true",
                     help="use the multi-GPU entry even with one rank (exercises E1-E9 on one GPU)")
     ap.add_argument("--lib", default=None, help="tuning only: load this libgbs build instead of the in-tree one")
@@ -226,8 +226,8 @@ def pin_one_core():
 def config_of(args, world: int) -> dict:
     """The workload's config dict -- identical for the GBS arm and the reference arm."""
     w = WORKLOADS[args.workload]
-    n = args.n or w["n"]
-    cfg = {"workload": w["name"] if not args.n else f"{args.workload} shape at n={args.n} (size override)",
+    n = args.size or w["n"]
+    cfg = {"workload": w["name"] if not args.size else f"{args.workload} shape at n={args.size} (size override)",
            "n_total": n, "items": "u32 key -> u32 value pairs" if w["pairs"] else "u32 keys",
            "dist": args.dist, "parallelism": f"dp{world}" if world > 1 else "single",
            "l2": "inputs > L2 and flushed between steps (256 MiB memset) outside the event window"}
@@ -252,7 +252,7 @@ def run_reference(args):
         return
     core = pin_one_core()
     w = WORKLOADS[args.workload]
-    n_full = args.n or w["n"]
+    n_full = args.size or w["n"]
     pairs = w["pairs"]
     n = min(n_full, 1 << 22)                        # bounded sample: ~1-2 s of CPU per step
     keys = gi.generate(args.dist, n, seed=0)
@@ -411,7 +411,7 @@ def main():
         return
 
     # ---------------- headline (N = 1)
-    n = args.n or w["n"]
+    n = args.size or w["n"]
     if args.ncu_one:
         keys = gi.generate_torch(args.dist, n, seed=0, device=dev)
         vals = torch.arange(n, dtype=torch.int32, device=dev) if pairs else None
@@ -446,7 +446,7 @@ def main():
     gc(torch, res)
 
     # ---------------- extras in the same run: C2, C3 x 7 distributions, the C5 base point
-    if not args.no_extras and not args.n:
+    if not args.no_extras and not args.size:
         c2 = run_single(args, torch, gi, gbs, dev, stream, flush, peak, WORKLOADS["C2"]["n"], False, "uniform",
                         args.steps, args.warmup)
         line["c2"] = {"workload": WORKLOADS["C2"]["name"], "value": c2["value"], "unit": "keys/s", "ms": c2["ms"],
@@ -629,7 +629,7 @@ def fingerprint(torch, t, chunk=1 << 27):
 
 
 def run_c5(args, torch, dist, gi, gbs, dev, world, rank, local, stream, flush, peak):
-    N = args.n or WORKLOADS["C5"]["n"]
+    N = args.size or WORKLOADS["C5"]["n"]
     n = N // world
     pristine = gi.generate_torch(args.dist, N, seed=0, device=dev, start=n * rank, count=n)
     keys = pristine.clone()

@@ -237,11 +237,12 @@ __global__ void k_p2p_barrier(u64* const* flags, int p, int rank, u64 epoch, uns
 // E9: k-way merge of the p runs received (recv, in source order) into out, one CTA per
 // chunk between consecutive sorted samples of this rank's bucket.  Run r of chunk j is
 // [F[r][q_j - 1], F[r][q_j]) - F[r][qlo] (relative to run r's start) with q_j = qlo + 1 + j.
-// Inside a chunk the CTA streams: it loads a window of up to TW items of every piece,
-// takes from each piece what is <= the smallest last-loaded item of the pieces that have
-// more to load (ties broken by run index: the merge is stable by source rank), merges the
-// taken pieces in shared memory (pairwise merge-path levels) and writes them out.
-constexpr int KM_BLOCK = 512, KM_ITEMS = 8, KM_CAP = KM_BLOCK * KM_ITEMS;   // 4096 items per window
+// Inside a chunk the CTA streams: it loads a window of up to TW = CAP/p items of every
+// piece (one batch of loads, all in flight), takes from each piece what is <= the smallest
+// last-loaded item of the pieces that have more to load (ties broken by run index: the
+// merge is stable by source rank), merges the taken pieces in shared memory (pairwise
+// merge-path levels, piece table in shared memory) and writes them out coalesced.
+constexpr int KM_BLOCK = 512, KM_ITEMS = 16, KM_CAP = KM_BLOCK * KM_ITEMS;   // 8192 items per window
 
 __device__ __forceinline__ int merge_split(const uint32_t* A, int na, const uint32_t* B, int nb, int diag)
 {
@@ -257,10 +258,15 @@ __device__ __forceinline__ int merge_split(const uint32_t* A, int na, const uint
 __global__ void __launch_bounds__(KM_BLOCK) k_kway_merge(const uint32_t* recv, const u64* F, uint32_t nq, uint32_t s_r,
                                                          int p, int rank, uint32_t* out, u64* n_out)
 {
-    __shared__ uint32_t bufA[KM_CAP], bufB[KM_CAP];
+    extern __shared__ __align__(16) uint32_t km_smem[];
+    uint32_t* bufA = km_smem;
+    uint32_t* bufB = km_smem + KM_CAP;
     __shared__ u64 s_base[MERGE_MAX_P], s_lo[MERGE_MAX_P], s_hi[MERGE_MAX_P];
-    __shared__ int s_take[MERGE_MAX_P + 1], s_win[MERGE_MAX_P], s_off[MERGE_MAX_P + 1];
+    __shared__ int s_win[MERGE_MAX_P];
+    // piece table per merge level: offset and length of every piece (level 0 = the windows)
+    __shared__ int s_poff[5][MERGE_MAX_P + 1], s_plen[5][MERGE_MAX_P + 1];
     __shared__ u64 s_o;
+    __shared__ int s_more;
     const int tw = KM_CAP / p;                                   // window per piece
     const long long qlo = (long long)rank * s_r - 1;
     const long long qj = qlo + 1 + blockIdx.x;
@@ -279,15 +285,31 @@ __global__ void __launch_bounds__(KM_BLOCK) k_kway_merge(const uint32_t* recv, c
     }
     __syncthreads();
     while (true) {
-        // load a window of every piece (piece r at bufA[r tw ...])
-        bool more = false;
-        for (int r = 0; r < p; ++r) more |= s_lo[r] < s_hi[r];
-        if (!more) break;
-        for (int r = 0; r < p; ++r) {
-            const int w = (int)min((u64)tw, s_hi[r] - s_lo[r]);
-            const uint32_t* src = recv + s_base[r] + s_lo[r];
-            for (int i = threadIdx.x; i < w; i += KM_BLOCK) bufA[r * tw + i] = src[i];
-            if (threadIdx.x == 0) s_win[r] = w;
+        if (threadIdx.x == 0) {
+            int more = 0;
+            for (int r = 0; r < p; ++r) {
+                const int w = (int)min((u64)tw, s_hi[r] - s_lo[r]);
+                s_win[r] = w;
+                more |= w > 0;
+            }
+            s_more = more;
+        }
+        __syncthreads();
+        if (!s_more) break;
+        {   // the windows of all pieces in one batch of loads (piece r at bufA[r tw ...])
+            uint32_t v[KM_ITEMS];
+#pragma unroll
+            for (int k = 0; k < KM_ITEMS; ++k) {
+                const int i = threadIdx.x + k * KM_BLOCK;
+                const int r = i / tw, j = i - r * tw;
+                v[k] = (r < p && j < s_win[r]) ? __ldg(recv + s_base[r] + s_lo[r] + j) : 0u;
+            }
+#pragma unroll
+            for (int k = 0; k < KM_ITEMS; ++k) {
+                const int i = threadIdx.x + k * KM_BLOCK;
+                const int r = i / tw, j = i - r * tw;
+                if (r < p && j < s_win[r]) bufA[i] = v[k];
+            }
         }
         __syncthreads();
         if (threadIdx.x < 32) {
@@ -316,66 +338,72 @@ __global__ void __launch_bounds__(KM_BLOCK) k_kway_merge(const uint32_t* recv, c
                     }
                     t = lo;
                 }
-                s_take[r] = t;
+                s_plen[0][r] = t;
+                s_poff[0][r] = r * tw;
             }
             __syncwarp();
-            if (lane == 0) {
-                int o = 0;
-                for (int r = 0; r < p; ++r) { s_off[r] = o; o += s_take[r]; }
-                s_off[p] = o;
+            if (lane == 0) {   // the piece tables of the merge levels
+                int np = p, lev = 0;
+                while (np > 1) {
+                    const int nn = (np + 1) / 2;
+                    int o = 0;
+                    for (int i = 0; i < nn; ++i) {
+                        const int len = s_plen[lev][2 * i] + (2 * i + 1 < np ? s_plen[lev][2 * i + 1] : 0);
+                        s_poff[lev + 1][i] = o;
+                        s_plen[lev + 1][i] = len;
+                        o += len;
+                    }
+                    s_poff[lev + 1][nn] = o;
+                    np = nn;
+                    ++lev;
+                }
+                int T = 0;
+                for (int r = 0; r < p; ++r) T += s_plen[0][r];
+                s_poff[0][MERGE_MAX_P] = T;
             }
         }
         __syncthreads();
-        const int T = s_off[p];
-        // pieces of the current level: (buffer, offset, length); level 0 reads bufA at r*tw
-        int np = p;
+        const int T = s_poff[0][MERGE_MAX_P];
         uint32_t* cur = bufA;
         uint32_t* nxt = bufB;
-        int poff[MERGE_MAX_P + 1], plen[MERGE_MAX_P];
-        for (int r = 0; r < p; ++r) { poff[r] = r * tw; plen[r] = s_take[r]; }
+        int np = p, lev = 0;
         while (np > 1) {
-            // merge pieces (2i, 2i+1) -> piece i of the next level, output at its prefix
+            // merge pieces (2i, 2i+1) of level lev -> piece i of level lev+1
             const int nn = (np + 1) / 2;
-            int noff[MERGE_MAX_P], nlen[MERGE_MAX_P], o = 0;
-            for (int i = 0; i < nn; ++i) {
-                noff[i] = o;
-                nlen[i] = plen[2 * i] + (2 * i + 1 < np ? plen[2 * i + 1] : 0);
-                o += nlen[i];
-            }
-            {
-                // this thread's outputs [q, q1) may straddle two output pieces
-                int q = threadIdx.x * KM_ITEMS, i = 0;
-                const int q1 = min(T, q + KM_ITEMS);
-                while (q < q1) {
-                    while (i + 1 < nn && noff[i + 1] <= q) ++i;
-                    const uint32_t* Ai = cur + poff[2 * i];
-                    const int nai = plen[2 * i];
-                    const uint32_t* Bi = 2 * i + 1 < np ? cur + poff[2 * i + 1] : Ai + nai;
-                    const int nbi = 2 * i + 1 < np ? plen[2 * i + 1] : 0;
-                    const int qe = min(q1, noff[i] + nlen[i]);
-                    int ia = merge_split(Ai, nai, Bi, nbi, q - noff[i]);
-                    int ib = q - noff[i] - ia;
-                    for (; q < qe; ++q) {
-                        const bool ta = ia < nai && (ib >= nbi || Ai[ia] <= Bi[ib]);   // ties: lower run first
-                        nxt[q] = ta ? Ai[ia] : Bi[ib];
-                        ia += ta ? 1 : 0;
-                        ib += ta ? 0 : 1;
-                    }
+            int q = threadIdx.x * KM_ITEMS, i = 0;
+            const int q1 = min(T, q + KM_ITEMS);
+            while (q < q1) {   // this thread's outputs may straddle two output pieces
+                while (i + 1 < nn && s_poff[lev + 1][i + 1] <= q) ++i;
+                const uint32_t* Ai = cur + s_poff[lev][2 * i];
+                const int nai = s_plen[lev][2 * i];
+                const bool hasb = 2 * i + 1 < np;
+                const uint32_t* Bi = hasb ? cur + s_poff[lev][2 * i + 1] : Ai + nai;
+                const int nbi = hasb ? s_plen[lev][2 * i + 1] : 0;
+                const int o0 = s_poff[lev + 1][i];
+                const int qe = min(q1, o0 + s_plen[lev + 1][i]);
+                int ia = merge_split(Ai, nai, Bi, nbi, q - o0);
+                int ib = q - o0 - ia;
+                for (; q < qe; ++q) {
+                    const bool ta = ia < nai && (ib >= nbi || Ai[ia] <= Bi[ib]);   // ties: lower run first
+                    nxt[q] = ta ? Ai[ia] : Bi[ib];
+                    ia += ta ? 1 : 0;
+                    ib += ta ? 0 : 1;
                 }
             }
             __syncthreads();
-            np = nn;
-            for (int r = 0; r < np; ++r) { poff[r] = noff[r]; plen[r] = nlen[r]; }
             uint32_t* t = cur;
             cur = nxt;
             nxt = t;
+            np = nn;
+            ++lev;
         }
-        // write out: the single piece at poff[0] of cur (level 0 with p = 1: bufA)
+        // write out: the single piece of the last level (p = 1: the window itself)
         const u64 o0 = s_o;
-        for (int i = threadIdx.x; i < T; i += KM_BLOCK) out[o0 + i] = cur[poff[0] + i];
+        const int off = s_poff[lev][0];
+        for (int i = threadIdx.x; i < T; i += KM_BLOCK) out[o0 + i] = cur[off + i];
         __syncthreads();
         if (threadIdx.x == 0) {
-            for (int r = 0; r < p; ++r) s_lo[r] += s_take[r];
+            for (int r = 0; r < p; ++r) s_lo[r] += s_plen[0][r];
             s_o = o0 + T;
         }
         __syncthreads();
@@ -554,8 +582,10 @@ gbs_status_t phase_push(const RankCtx& c, uint32_t* const* d_recv)
 // E9 k-way merge recv -> out; n_out into words[0]
 gbs_status_t phase_merge(const RankCtx& c)
 {
-    k_kway_merge<<<c.s_r, KM_BLOCK, 0, c.st>>>(at<uint32_t>(c.win, c.W.recv), at<u64>(c.win, c.W.fcut), c.nq, c.s_r, c.p,
-                                              c.rank, c.out, c.words);
+    // 64 KB of dynamic shared memory (a per-device attribute: set on every call, cheap)
+    cudaFuncSetAttribute(k_kway_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * KM_CAP * 4);
+    k_kway_merge<<<c.s_r, KM_BLOCK, 2 * KM_CAP * 4, c.st>>>(at<uint32_t>(c.win, c.W.recv), at<u64>(c.win, c.W.fcut), c.nq,
+                                                           c.s_r, c.p, c.rank, c.out, c.words);
     CUDA_OK(cudaGetLastError());
     return GBS_SUCCESS;
 }

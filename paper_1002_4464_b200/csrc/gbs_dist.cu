@@ -243,24 +243,29 @@ __global__ void k_p2p_barrier(u64* const* flags, int p, int rank, u64 epoch, uns
 // merge is stable by source rank), merges the taken pieces in shared memory (pairwise
 // merge-path levels, piece table in shared memory) and writes them out coalesced.
 constexpr int KM_BLOCK = 512, KM_ITEMS = 16, KM_CAP = KM_BLOCK * KM_ITEMS;   // 8192 items per window
+// shared-memory layout with one pad slot per KM_ITEMS: a thread's KM_ITEMS consecutive
+// outputs then sit at stride KM_ITEMS + 1 across the warp (conflict-free stores)
+constexpr int KM_PAD_CAP = KM_CAP + KM_CAP / KM_ITEMS + 16;
+__device__ __forceinline__ int km_pad(int i) { return i + (i >> 4); }
 
-__device__ __forceinline__ int merge_split(const uint32_t* A, int na, const uint32_t* B, int nb, int diag)
+// merge-path split of diagonal `diag` of A = s[ao, ao+na) and B = s[bo, bo+nb) (padded)
+__device__ __forceinline__ int merge_split_pad(const uint32_t* s, int ao, int na, int bo, int nb, int diag)
 {
     int lo = max(0, diag - nb), hi = min(diag, na);
     while (lo < hi) {
         const int mid = (lo + hi) >> 1;
-        if (A[mid] <= B[diag - 1 - mid]) lo = mid + 1;
+        if (s[km_pad(ao + mid)] <= s[km_pad(bo + diag - 1 - mid)]) lo = mid + 1;
         else hi = mid;
     }
     return lo;
 }
 
-__global__ void __launch_bounds__(KM_BLOCK) k_kway_merge(const uint32_t* recv, const u64* F, uint32_t nq, uint32_t s_r,
+__global__ void __launch_bounds__(KM_BLOCK, 2) k_kway_merge(const uint32_t* recv, const u64* F, uint32_t nq, uint32_t s_r,
                                                          int p, int rank, uint32_t* out, u64* n_out)
 {
     extern __shared__ __align__(16) uint32_t km_smem[];
     uint32_t* bufA = km_smem;
-    uint32_t* bufB = km_smem + KM_CAP;
+    uint32_t* bufB = km_smem + KM_PAD_CAP;
     __shared__ u64 s_base[MERGE_MAX_P], s_lo[MERGE_MAX_P], s_hi[MERGE_MAX_P];
     __shared__ int s_win[MERGE_MAX_P];
     // piece table per merge level: offset and length of every piece (level 0 = the windows)
@@ -308,7 +313,7 @@ __global__ void __launch_bounds__(KM_BLOCK) k_kway_merge(const uint32_t* recv, c
             for (int k = 0; k < KM_ITEMS; ++k) {
                 const int i = threadIdx.x + k * KM_BLOCK;
                 const int r = i / tw, j = i - r * tw;
-                if (r < p && j < s_win[r]) bufA[i] = v[k];
+                if (r < p && j < s_win[r]) bufA[km_pad(i)] = v[k];
             }
         }
         __syncthreads();
@@ -319,7 +324,7 @@ __global__ void __launch_bounds__(KM_BLOCK) k_kway_merge(const uint32_t* recv, c
             int tr = MERGE_MAX_P;                                 // MERGE_MAX_P = no threshold
             for (int r = 0; r < p; ++r) {
                 if (s_lo[r] + s_win[r] < s_hi[r]) {
-                    const uint32_t k = bufA[r * tw + s_win[r] - 1];
+                    const uint32_t k = bufA[km_pad(r * tw + s_win[r] - 1)];
                     if (tr == MERGE_MAX_P || k < tk) { tk = k; tr = r; }
                 }
             }
@@ -328,11 +333,11 @@ __global__ void __launch_bounds__(KM_BLOCK) k_kway_merge(const uint32_t* recv, c
                 const int r = lane, w = s_win[r];
                 int t = w;
                 if (tr != MERGE_MAX_P && r != tr) {
-                    const uint32_t* a = bufA + r * tw;
                     int lo = 0, hi = w;
                     while (lo < hi) {
                         const int mid = (lo + hi) >> 1;
-                        const bool take = r < tr ? a[mid] <= tk : a[mid] < tk;
+                        const uint32_t am = bufA[km_pad(r * tw + mid)];
+                        const bool take = r < tr ? am <= tk : am < tk;
                         if (take) lo = mid + 1;
                         else hi = mid;
                     }
@@ -374,20 +379,26 @@ __global__ void __launch_bounds__(KM_BLOCK) k_kway_merge(const uint32_t* recv, c
             const int q1 = min(T, q + KM_ITEMS);
             while (q < q1) {   // this thread's outputs may straddle two output pieces
                 while (i + 1 < nn && s_poff[lev + 1][i + 1] <= q) ++i;
-                const uint32_t* Ai = cur + s_poff[lev][2 * i];
+                const int ao = s_poff[lev][2 * i];
                 const int nai = s_plen[lev][2 * i];
                 const bool hasb = 2 * i + 1 < np;
-                const uint32_t* Bi = hasb ? cur + s_poff[lev][2 * i + 1] : Ai + nai;
+                const int bo = hasb ? s_poff[lev][2 * i + 1] : ao + nai;
                 const int nbi = hasb ? s_plen[lev][2 * i + 1] : 0;
                 const int o0 = s_poff[lev + 1][i];
                 const int qe = min(q1, o0 + s_plen[lev + 1][i]);
-                int ia = merge_split(Ai, nai, Bi, nbi, q - o0);
+                int ia = merge_split_pad(cur, ao, nai, bo, nbi, q - o0);
                 int ib = q - o0 - ia;
+                uint32_t a = ia < nai ? cur[km_pad(ao + ia)] : 0u, b = ib < nbi ? cur[km_pad(bo + ib)] : 0u;
                 for (; q < qe; ++q) {
-                    const bool ta = ia < nai && (ib >= nbi || Ai[ia] <= Bi[ib]);   // ties: lower run first
-                    nxt[q] = ta ? Ai[ia] : Bi[ib];
-                    ia += ta ? 1 : 0;
-                    ib += ta ? 0 : 1;
+                    const bool ta = ia < nai && (ib >= nbi || a <= b);   // ties: lower run first
+                    nxt[km_pad(q)] = ta ? a : b;
+                    if (ta) {
+                        ++ia;
+                        if (ia < nai) a = cur[km_pad(ao + ia)];
+                    } else {
+                        ++ib;
+                        if (ib < nbi) b = cur[km_pad(bo + ib)];
+                    }
                 }
             }
             __syncthreads();
@@ -400,7 +411,7 @@ __global__ void __launch_bounds__(KM_BLOCK) k_kway_merge(const uint32_t* recv, c
         // write out: the single piece of the last level (p = 1: the window itself)
         const u64 o0 = s_o;
         const int off = s_poff[lev][0];
-        for (int i = threadIdx.x; i < T; i += KM_BLOCK) out[o0 + i] = cur[off + i];
+        for (int i = threadIdx.x; i < T; i += KM_BLOCK) out[o0 + i] = cur[km_pad(off + i)];
         __syncthreads();
         if (threadIdx.x == 0) {
             for (int r = 0; r < p; ++r) s_lo[r] += s_plen[0][r];
@@ -583,8 +594,8 @@ gbs_status_t phase_push(const RankCtx& c, uint32_t* const* d_recv)
 gbs_status_t phase_merge(const RankCtx& c)
 {
     // 64 KB of dynamic shared memory (a per-device attribute: set on every call, cheap)
-    cudaFuncSetAttribute(k_kway_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * KM_CAP * 4);
-    k_kway_merge<<<c.s_r, KM_BLOCK, 2 * KM_CAP * 4, c.st>>>(at<uint32_t>(c.win, c.W.recv), at<u64>(c.win, c.W.fcut), c.nq,
+    cudaFuncSetAttribute(k_kway_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * KM_PAD_CAP * 4);
+    k_kway_merge<<<c.s_r, KM_BLOCK, 2 * KM_PAD_CAP * 4, c.st>>>(at<uint32_t>(c.win, c.W.recv), at<u64>(c.win, c.W.fcut), c.nq,
                                                            c.s_r, c.p, c.rank, c.out, c.words);
     CUDA_OK(cudaGetLastError());
     return GBS_SUCCESS;

@@ -160,6 +160,11 @@ struct Node {
 #endif
 #define GBS_BIG_KEYS GBS_KEYS_BLOCK, GBS_KEYS_ITEMS
 #define GBS_BIG_WIDE GBS_WIDE_BLOCK, GBS_WIDE_ITEMS
+#ifndef GBS_PAIRS_LOCAL_BLOCK
+#define GBS_PAIRS_LOCAL_BLOCK GBS_WIDE_BLOCK   // Step 2 of pairs (A/B: 512 x 32)
+#define GBS_PAIRS_LOCAL_ITEMS GBS_WIDE_ITEMS
+#endif
+#define GBS_PAIRS_LOCAL GBS_PAIRS_LOCAL_BLOCK, GBS_PAIRS_LOCAL_ITEMS
 #ifndef GBS_SMALL
 #define GBS_SMALL 256, 8
 #endif
@@ -547,6 +552,7 @@ static void launch_local(const LevelDev& lv, bool small, cudaStream_t st)
 {
     if (small) launch_local_t<KIND, GBS_SMALL>(lv, st);
     else if constexpr (KIND == KIND_KEYS) launch_local_t<KIND, GBS_BIG_KEYS>(lv, st);
+    else if constexpr (KIND == KIND_PAIRS) launch_local_t<KIND, GBS_PAIRS_LOCAL>(lv, st);
     else launch_local_t<KIND, GBS_BIG_WIDE>(lv, st);
 }
 

@@ -9,7 +9,7 @@
 Timing: input restored from a pristine copy outside the CUDA-event window, 3 warm-ups,
 median of `--reps` sorts.  Every sorted output is checked against torch.sort.
 
-usage: python scripts/experiments.py [--reps 10] [--out profiles/r01c/experiments]"""
+usage: python scripts/experiments.py [--reps 10] [--out profiles/r02/experiments]"""
 import argparse
 import json
 import os
@@ -56,6 +56,7 @@ def time_sort(keys_np, cfg=None, reps=10, prof=False):
            "plan": gbs.plan(n, cfg=cfg)["levels"]}
     if steps:
         calls = steps.pop("calls")
+        steps.pop("level", None)
         out["steps_ms"] = {k: round(v / calls, 4) for k, v in steps.items()}
     return out
 
@@ -66,7 +67,7 @@ def main():
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "experiments"))
     args = ap.parse_args()
     res = {"device": torch.cuda.get_device_name(0), "fig3_n_scaling": [], "fig5_s_sweep": []}
-    for lg in (16, 18, 20, 22, 24, 25, 26, 27, 28):
+    for lg in (16, 18, 20, 22, 24, 25, 26, 27, 28, 29, 30, 31):
         n = 1 << lg
         r = time_sort(gi.generate("uniform", n, seed=0), reps=args.reps)
         res["fig3_n_scaling"].append(r)

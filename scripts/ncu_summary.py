@@ -99,13 +99,20 @@ def main():
                 key = f"{label}:{base}"
             e = summary["kernels"].get(key)
             if e is None or e.get("_rep") != rep:
-                e = dict(d, launches=1, parts=[d["kernel"]], _rep=rep)
+                e = dict(d, launches=1, parts=[d["kernel"]], _rep=rep, _longest=d.get("gpu__time_duration.sum", 0))
                 summary["kernels"][key] = e
             else:
-                # a step issued as several launches of one step kernel: sum traffic and time
+                # a step issued as several launches of one step kernel: sum traffic and time;
+                # the utilisation and stall figures are those of its longest launch
+                longest = d.get("gpu__time_duration.sum", 0) > e.get("_longest", 0)
                 for w in SUM:
                     if isinstance(d.get(w), float):
                         e[w] = e.get(w, 0.0) + d[w]
+                if longest:
+                    for w, v in d.items():
+                        if w not in SUM and w != "kernel":
+                            e[w] = v
+                    e["_longest"] = d.get("gpu__time_duration.sum", 0)
                 e["launches"] += 1
                 e["parts"].append(d["kernel"])
             e["dram_bytes_one_launch"] = e.get("dram__bytes_read.sum", 0) + e.get("dram__bytes_write.sum", 0)
@@ -113,6 +120,7 @@ def main():
             e["capture"] = f"ncu --set full, {label}, first sort of the bench command"
     for e in summary["kernels"].values():
         e.pop("_rep", None)
+        e.pop("_longest", None)
     open(out_path, "w").write(json.dumps(summary, indent=1))
     for k, e in summary["kernels"].items():
         print(f"{k:40s} {e.get('duration_us', 0):10.1f} us  DRAM {e['dram_bytes_one_launch'] / 1e6:9.1f} MB  "

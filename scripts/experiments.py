@@ -67,7 +67,7 @@ def main():
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "experiments"))
     args = ap.parse_args()
     res = {"device": torch.cuda.get_device_name(0), "fig3_n_scaling": [], "fig5_s_sweep": []}
-    for lg in (16, 18, 20, 22, 24, 25, 26, 27, 28, 29, 30, 31):
+    for lg in (16, 18, 20, 22, 24, 25, 26, 27, 28, 29, 30):   # (2^31: bench.py c5_base)
         n = 1 << lg
         r = time_sort(gi.generate("uniform", n, seed=0), reps=args.reps)
         res["fig3_n_scaling"].append(r)

@@ -389,14 +389,14 @@ __global__ void __launch_bounds__(KM_BLOCK, 2) k_kway_merge(const uint32_t* recv
                 int ia = merge_split_pad(cur, ao, nai, bo, nbi, q - o0);
                 int ib = q - o0 - ia;
                 uint32_t a = ia < nai ? cur[km_pad(ao + ia)] : 0u, b = ib < nbi ? cur[km_pad(bo + ib)] : 0u;
-                for (; q < qe; ++q) {   // branch-free: one (predicated) load per output
-                    const bool ta = ia < nai && (ib >= nbi || a <= b);   // ties: lower run first
+                for (; q < qe; ++q) {   // branch-free: one load per output
+                    // ties: lower run first; an exhausted run is never taken (the load one
+                    // past its end reads the buffer's next slot, within the slack)
+                    const bool ta = ib >= nbi || (ia < nai && a <= b);
                     nxt[km_pad(q)] = ta ? a : b;
                     ia += ta ? 1 : 0;
                     ib += ta ? 0 : 1;
-                    const int nidx = ta ? ao + ia : bo + ib;
-                    const bool ok = ta ? ia < nai : ib < nbi;
-                    const uint32_t v = cur[km_pad(ok ? nidx : ao)];
+                    const uint32_t v = cur[km_pad(ta ? ao + ia : bo + ib)];
                     a = ta ? v : a;
                     b = ta ? b : v;
                 }

@@ -96,12 +96,6 @@ constexpr uint32_t SMALL_TILE = 2048;      // small CTA configuration
 #ifndef GBS_FUSE_PAIRS
 #define GBS_FUSE_PAIRS 1  // ... for pairs as well (C4: 81.6 -> 80.8 ms)
 #endif
-#ifndef GBS_FUSE_NEXT_PAIRS
-#define GBS_FUSE_NEXT_PAIRS 1  // nested pairs levels gather from the sorted sublists (R27)
-#endif
-#ifndef GBS_FUSE_NEXT_KEYS
-#define GBS_FUSE_NEXT_KEYS 0   // ... keys (A/B)
-#endif
 #ifndef GBS_FUSE_MIN_D
 #define GBS_FUSE_MIN_D 32 // ... whose average run d = L/s is at least this many items
 #endif
@@ -151,8 +145,6 @@ struct Node {
     bool s4_tree = false; // Step 4 as a merge tree (R22) instead of a u64 level
     int s4_levels = 0;    // its global merge levels (between the tile merge and the selection)
     int level = 0;        // 0 top, k nested Step 9 level k, -1 a Step 4 sample level (profiling)
-    bool fuse_next = false;   // R27: no Step 8; the nested level gathers from the sorted sublists
-    size_t o_runs = 0;        // ... through the transposed run table (2 x s x (m + 1) u32)
     size_t o_s4tmp = 0;   // its ping-pong buffer (m*s u64)
 };
 
@@ -387,14 +379,7 @@ static int build_node(Plan& P, int kind, uint32_t B, uint64_t N, uint32_t pad_ba
     } else {
         P.nodes[idx].o_child_off = P.alloc((uint64_t)B * s * 8);
         P.nodes[idx].o_child_len = P.alloc((uint64_t)B * s * 4);
-        // R27: a top-level node's nested Step 2 may read its buckets straight from the
-        // sorted sublists (no Step 8 pass; a transposed run table instead)
-        const bool fnext = B == 1 && ((kind == KIND_PAIRS && GBS_FUSE_NEXT_PAIRS) || (kind == KIND_KEYS && GBS_FUSE_NEXT_KEYS));
-        if (fnext) {
-            P.nodes[idx].fuse_next = true;
-            P.nodes[idx].o_runs = P.alloc(2 * (uint64_t)s * ((uint64_t)nd.m + 1) * 4);
-        }
-        P.launches += (fnext ? 1 : reloc_launches(kind)) + 1;  // relocate (or run table) + child descriptors
+        P.launches += reloc_launches(kind) + 1;  // relocate + child descriptors
         const uint64_t nb = (uint64_t)B * s;
         if (nb >= (1ull << 31)) { snprintf(g_err, sizeof g_err, "too many nested problems"); return -1; }
         const int c9 = build_node(P, kind, (uint32_t)nb, nd.hi, child_pad, nullptr, false, level >= 0 ? level + 1 : -1);
@@ -436,11 +421,11 @@ constexpr int S4_MERGE_BLOCK = 256, S4_MERGE_ITEMS = 16;
 // kernel may launch while its predecessor on the stream drains (each kernel waits on
 // griddepcontrol.wait before touching global memory; pdl_entry in gbs_kernels.cuh).
 template <typename... KArgs, typename... Args>
-static void launch_k(void (*kernel)(KArgs...), dim3 grid, unsigned block, size_t smem, cudaStream_t st,
+static void launch_k(void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
                      Args&&... args)
 {
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = grid;
+    cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(block);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
@@ -715,12 +700,6 @@ struct Bufs {
     void* srt = nullptr;
     // typed keys: transform at the first level's loads / the last level's stores
     int xf_in = 0, xf_out = 0;
-    // R27: a nested level fed from the level above's sorted sublists (run table)
-    const uint32_t* g_lrel = nullptr;
-    const uint32_t* g_src = nullptr;
-    uint32_t g_stride = 0;
-    const void* g_keys = nullptr;
-    const uint32_t* g_vals = nullptr;
 };
 
 template <int KIND>
@@ -928,11 +907,6 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
     lv.presorted = pr.presorted;
     lv.xf_in = bf.xf_in;
     lv.xf_out = (nd.leaf || nd.step9 < 0) ? bf.xf_out : 0;
-    lv.g_lrel = bf.g_lrel;
-    lv.g_src = bf.g_src;
-    lv.g_stride = bf.g_stride;
-    lv.g_keys = bf.g_keys;
-    lv.g_vals = bf.g_vals;
     lv.seg_min = 0;
     lv.seg_max = 0xFFFFFFFFu;
     if (nd.leaf) {
@@ -1058,10 +1032,8 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
     if (stop == 7) return GBS_SUCCESS;
     pm.mark();
 
-    // Step 8: relocation in -> reloc (fused into Step 9 on the production path, or into the
-    // nested level's Step 2, R27)
-    const bool fnext = nd.fuse_next && stop == 0;
-    if (!fuse && !fnext) {
+    // Step 8: relocation in -> reloc (fused into Step 9 on the production path)
+    if (!fuse) {
         launch_relocate<KIND>(lv, st);
         GBS_LAUNCHED();
     }
@@ -1127,20 +1099,6 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
         // sublists' buffer (dead after Step 8) as its own relocation target
         Bufs b9{bf.reloc, bf.srt ? bf.srt : bf.in, bf.out, bf.reloc_v, bf.in_v, bf.out_v};
         b9.xf_out = bf.xf_out;   // the keys entered the sort at this level's Step 2
-        if (fnext) {
-            // R27: its Step 2 gathers every sublist from the runs of the bucket above
-            // (stream order: the sorted sublists are complete, and only the nested Step 2
-            // reads them before the nested level writes its own relocation / output)
-            uint32_t* lrelT = reinterpret_cast<uint32_t*>(ws + nd.o_runs);
-            uint32_t* srcT = lrelT + (uint64_t)nd.s * ((uint64_t)nd.m + 1);
-            launch_k(k_runs_transpose, dim3((nd.s + 31) / 32, (nd.m + 31) / 32), 256, 0, st, lv, lrelT, srcT);
-            GBS_LAUNCHED();
-            b9.g_lrel = lrelT;
-            b9.g_src = srcT;
-            b9.g_stride = nd.m + 1;
-            b9.g_keys = lv.srt;
-            b9.g_vals = lv.srt_v;
-        }
         Probs p9{lv.child_off, lv.child_len, 0, 0};
         gbs_status_t r = exec(P, nd.step9, ws, b9, p9, st, 0);
         if (r) return r;

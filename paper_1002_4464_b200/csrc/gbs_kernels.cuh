@@ -92,15 +92,6 @@ struct LevelDev {
     // typed keys: the transform applied where keys enter (Step 2 / leaf loads from `in`)
     // and leave (the last level's Step 9 / leaf stores to `out`); 0 = none
     int xf_in, xf_out;
-    // nested level fed straight from the level above's sorted sublists (its Step 8
-    // skipped, R27): for problem b (bucket b above), g_lrel[b*g_stride + r] = where run r
-    // of the bucket starts in bucket order (entry g_stride-1 = the bucket's length) and
-    // g_src[b*g_stride + r] + p = the item of bucket position p inside run r
-    const uint32_t* g_lrel;
-    const uint32_t* g_src;
-    uint32_t g_stride;
-    const void* g_keys;
-    const uint32_t* g_vals;
 };
 
 // L2 prefetch of a byte range (cp.async.bulk.prefetch: a TMA bulk operation, no
@@ -243,50 +234,6 @@ struct Seg {
             for (int k = 0; k < ITEMS; ++k) x[k] = 32 * k < rem ? xf_in(s[p0 + 32 * k], xf) : CS::TMAX;
         } else {
             CS::load(x, reinterpret_cast<const KeyT*>(src) + off, v);
-        }
-    }
-
-    // Nested Step 2 fed from the level above (R27): slot k holds position
-    // pos0 + load_pos(k) of problem b (a bucket above, in its relocation order), read from
-    // the run it falls in: one bisection over the bucket's run starts for the lane's
-    // first position, then a forward walk (positions only grow by 32).
-    template <int M>
-    static __device__ __forceinline__ void load_runs(T (&x)[M], const LevelDev& lv, uint32_t b, uint32_t pos0, int v,
-                                                     unsigned char* smem)
-    {
-        const uint32_t* lrel = lv.g_lrel + (uint64_t)b * lv.g_stride;
-        const uint32_t* src = lv.g_src + (uint64_t)b * lv.g_stride;
-        const int p0 = CS::load_pos(0);
-        int r = 0;
-        if (p0 < v) {
-            int lo = 0, hi = (int)lv.g_stride - 2;            // last run r with lrel[r] <= P
-            const uint32_t P = pos0 + (uint32_t)p0;
-            while (lo < hi) {
-                const int mid = (lo + hi + 1) >> 1;
-                if (__ldg(lrel + mid) <= P) lo = mid;
-                else hi = mid - 1;
-            }
-            r = lo;
-        }
-        uint32_t nxt = __ldg(lrel + r + 1);
-        uint32_t* vsm = KIND == KIND_PAIRS ? vsm_of(smem) : nullptr;
-#pragma unroll
-        for (int k = 0; k < ITEMS; ++k) {
-            const int p = p0 + 32 * k;
-            if (p < v) {
-                const uint32_t P = pos0 + (uint32_t)p;
-                while (P >= nxt) nxt = __ldg(lrel + (++r) + 1);
-                const uint32_t q = __ldg(src + r) + P;
-                if constexpr (KIND == KIND_PAIRS) {
-                    x[k] = ((T)__ldg(reinterpret_cast<const uint32_t*>(lv.g_keys) + q) << 32) | (T)(uint32_t)p;
-                    vsm[p] = __ldg(lv.g_vals + q);
-                } else {
-                    x[k] = (T)__ldg(reinterpret_cast<const KeyT*>(lv.g_keys) + q);
-                }
-            } else {
-                if constexpr (KIND == KIND_PAIRS) x[k] = ((T)0xFFFFFFFFu << 32) | (T)(uint32_t)p;
-                else x[k] = CS::TMAX;
-            }
         }
     }
 
@@ -473,23 +420,12 @@ __global__ void __launch_bounds__(BLOCK, 1) k_local_sort(LevelDev lv)
     const bool presorted = KIND == KIND_U64 && GBS_PRESORTED && lv.presorted >= (uint32_t)ITEMS;
     const bool pipe = KIND != KIND_PAIRS && !presorted;
     T x[ITEMS];
-    // a sublist's items: from `in`, or (nested level fed from the level above, R27)
-    // gathered from the runs of the bucket above
-    auto load = [&](uint32_t t, uint64_t st, int vv) {
-        if constexpr (KIND != KIND_U64) {
-            if (lv.g_lrel) {
-                S::load_runs(x, lv, t / lv.m, (t % lv.m) * lv.L, vv, smem_raw);
-                return;
-            }
-        }
-        S::load_regs(x, lv.in, lv.in_v, st, vv, smem_raw, lv.xf_in);
-    };
     uint32_t tile = lv.tile_lo + blockIdx.x;
     uint64_t start = 0;
     int v = 0;
     if (tile < ntiles) {
         sublist_of(lv, tile, start, v);
-        if (pipe) load(tile, start, v);
+        if (pipe) S::load_regs(x, lv.in, lv.in_v, start, v, smem_raw, lv.xf_in);
     }
     for (; tile < ntiles; tile += gridDim.x) {
         const uint32_t b = tile / lv.m, i = tile % lv.m;
@@ -500,7 +436,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_local_sort(LevelDev lv)
         int nv = 0;
         if (nxt < ntiles) {
             sublist_of(lv, nxt, nstart, nv);
-            if (threadIdx.x == 0 && !lv.g_lrel) {
+            if (threadIdx.x == 0) {
                 prefetch_l2(reinterpret_cast<const KeyT*>(lv.in) + nstart, (size_t)nv * sizeof(KeyT));
                 if (KIND == KIND_PAIRS) prefetch_l2(lv.in_v + nstart, (size_t)nv * 4);
             }
@@ -511,11 +447,11 @@ __global__ void __launch_bounds__(BLOCK, 1) k_local_sort(LevelDev lv)
                     S::CS::sort_presorted(x, reinterpret_cast<const unsigned long long*>(lv.in) + start, sm, v,
                                           (int)lv.presorted);
             } else {
-                if (!pipe) load(tile, start, v);
+                if (!pipe) S::load_regs(x, lv.in, lv.in_v, start, v, smem_raw, lv.xf_in);
                 S::CS::sort(x, sm, v);
             }
         }
-        if (pipe && nv > 0) load(nxt, nstart, nv);   // in flight during the store
+        if (pipe && nv > 0) S::load_regs(x, lv.in, lv.in_v, nstart, nv, smem_raw, lv.xf_in);   // in flight during the store
         if (v > 0) S::store(lv.srt, lv.srt_v, start, v, smem_raw);
         u64* smp = lv.samples + ((uint64_t)b * lv.m + i) * lv.s;
         for (uint32_t k = threadIdx.x; k < lv.s; k += BLOCK) {
@@ -1721,39 +1657,6 @@ __global__ void k_check_level(LevelDev lv, unsigned* flag, int only_splitters)
                 flag[6] = (unsigned)(g >> 32); flag[7] = (unsigned)g;
             }
         }
-    }
-}
-
-// R27: the run table of every bucket of a top-level node (B = 1), transposed so that each
-// bucket's m runs are contiguous: lrelT[j*(m+1) + r] = l_rj - l_0j (where run (r, j) starts
-// in bucket j), srcT[...] = r L + P_r,j-1 - that (so srcT + p is the sorted-sublist item of
-// bucket position p in run r), lrelT[j*(m+1) + m] = |B_j|.  32 x 32 tiles through shared
-// memory (coalesced on both sides).
-__global__ void __launch_bounds__(256) k_runs_transpose(LevelDev lv, uint32_t* lrelT, uint32_t* srcT)
-{
-    pdl_entry();
-    __shared__ uint32_t tl[32][33], ts[32][33];
-    const uint32_t j0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;   // 32 x 8
-    const uint32_t S = lv.s, m = lv.m;
-    for (int yy = ty; yy < 32; yy += 8) {
-        const uint32_t r = r0 + yy, j = j0 + tx;
-        if (r < m && j < S) {
-            const uint32_t lr = lv.l[(uint64_t)r * S + j] - lv.l[j];
-            tl[yy][tx] = lr;
-            ts[yy][tx] = r * lv.L + lv.pex[(uint64_t)r * S + j] - lr;
-        }
-    }
-    __syncthreads();
-    const uint64_t stride = (uint64_t)m + 1;
-    for (int yy = ty; yy < 32; yy += 8) {
-        const uint32_t j = j0 + yy, r = r0 + tx;
-        if (j < S && r < m) {
-            lrelT[j * stride + r] = tl[tx][yy];
-            srcT[j * stride + r] = ts[tx][yy];
-        }
-        if (j < S && blockIdx.y == 0 && tx == 0)
-            lrelT[j * stride + m] = (j + 1 < S ? lv.l[j + 1] : lv.pr.length(0)) - lv.l[j];
     }
 }
 

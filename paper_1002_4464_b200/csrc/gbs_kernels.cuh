@@ -212,21 +212,47 @@ struct Seg {
         return reinterpret_cast<uint32_t*>(reinterpret_cast<T*>(smem) + CS::SMEM_ELEMS);
     }
 
+    // Pairs: the keys of positions load_pos(k) as (key << 32 | position) composites (stable:
+    // ties by position) ...
+    template <int M>
+    static __device__ __forceinline__ void load_keys(T (&x)[M], const void* src, uint64_t off, int v, int xf = 0)
+    {
+        static_assert(KIND == KIND_PAIRS, "pairs only");
+        const int p0 = CS::load_pos(0), rem = v - p0;
+        const uint32_t* s = reinterpret_cast<const uint32_t*>(src) + off + p0;
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k) {
+            const uint32_t key = 32 * k < rem ? xf_in(__ldg(s + 32 * k), xf) : 0xFFFFFFFFu;
+            x[k] = ((T)key << 32) | (T)(uint32_t)(p0 + 32 * k);
+        }
+    }
+    // ... and their values parked in shared memory at their positions (gathered by position
+    // at the write-back): every load of the thread in flight before the stores
+    static __device__ __forceinline__ void load_vals(const uint32_t* src_v, uint64_t off, int v, unsigned char* smem)
+    {
+        uint32_t* vsm = vsm_of(smem);
+        const uint32_t* sv = src_v + off;
+        constexpr int PER = (TILE + BLOCK - 1) / BLOCK;
+        uint32_t t[PER];
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int p = (int)threadIdx.x + k * BLOCK;
+            t[k] = p < v ? __ldg(sv + p) : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int p = (int)threadIdx.x + k * BLOCK;
+            if (p < v) vsm[p] = t[k];
+        }
+    }
+
     template <int M>
     static __device__ __forceinline__ void load_regs(T (&x)[M], const void* src, const uint32_t* src_v,
                                                      uint64_t off, int v, unsigned char* smem, int xf = 0)
     {
         if constexpr (KIND == KIND_PAIRS) {
-            const int p0 = CS::load_pos(0), rem = v - p0;
-            const uint32_t* s = reinterpret_cast<const uint32_t*>(src) + off + p0;
-#pragma unroll
-            for (int k = 0; k < ITEMS; ++k) {
-                const uint32_t key = 32 * k < rem ? xf_in(__ldg(s + 32 * k), xf) : 0xFFFFFFFFu;
-                x[k] = ((T)key << 32) | (T)(uint32_t)(p0 + 32 * k);     // stable: ties by position
-            }
-            uint32_t* vsm = vsm_of(smem);
-            const uint32_t* sv = src_v + off;
-            for (int p = threadIdx.x; p < v; p += BLOCK) vsm[p] = __ldg(sv + p);
+            load_keys(x, src, off, v, xf);
+            load_vals(src_v, off, v, smem);
         } else if constexpr (KIND == KIND_KEYS) {
             const uint32_t* s = reinterpret_cast<const uint32_t*>(src) + off;
             const int p0 = CS::load_pos(0), rem = v - p0;     // load_pos(k) = p0 + 32k
@@ -418,14 +444,21 @@ __global__ void __launch_bounds__(BLOCK, 1) k_local_sort(LevelDev lv)
 
     const uint32_t ntiles = lv.tile_hi ? lv.tile_hi : lv.B * lv.m;
     const bool presorted = KIND == KIND_U64 && GBS_PRESORTED && lv.presorted >= (uint32_t)ITEMS;
-    const bool pipe = KIND != KIND_PAIRS && !presorted;
+    // the next sublist's items (pairs: keys) are loaded into the free registers while the
+    // current one is written back; pairs load their values before the sort (parked in
+    // shared memory, their latency overlaps the register phase of the sort)
+    const bool pipe = !presorted;
     T x[ITEMS];
     uint32_t tile = lv.tile_lo + blockIdx.x;
     uint64_t start = 0;
     int v = 0;
+    auto load_next = [&](uint64_t st, int vv) {   // into registers (pairs: the keys)
+        if constexpr (KIND == KIND_PAIRS) S::load_keys(x, lv.in, st, vv, lv.xf_in);
+        else S::load_regs(x, lv.in, lv.in_v, st, vv, smem_raw, lv.xf_in);
+    };
     if (tile < ntiles) {
         sublist_of(lv, tile, start, v);
-        if (pipe) S::load_regs(x, lv.in, lv.in_v, start, v, smem_raw, lv.xf_in);
+        if (pipe) load_next(start, v);
     }
     for (; tile < ntiles; tile += gridDim.x) {
         const uint32_t b = tile / lv.m, i = tile % lv.m;
@@ -447,11 +480,11 @@ __global__ void __launch_bounds__(BLOCK, 1) k_local_sort(LevelDev lv)
                     S::CS::sort_presorted(x, reinterpret_cast<const unsigned long long*>(lv.in) + start, sm, v,
                                           (int)lv.presorted);
             } else {
-                if (!pipe) S::load_regs(x, lv.in, lv.in_v, start, v, smem_raw, lv.xf_in);
+                if constexpr (KIND == KIND_PAIRS) S::load_vals(lv.in_v, start, v, smem_raw);
                 S::CS::sort(x, sm, v);
             }
         }
-        if (pipe && nv > 0) S::load_regs(x, lv.in, lv.in_v, nstart, nv, smem_raw, lv.xf_in);   // in flight during the store
+        if (pipe && nv > 0) load_next(nstart, nv);   // in flight during the store
         if (v > 0) S::store(lv.srt, lv.srt_v, start, v, smem_raw);
         u64* smp = lv.samples + ((uint64_t)b * lv.m + i) * lv.s;
         for (uint32_t k = threadIdx.x; k < lv.s; k += BLOCK) {

@@ -152,6 +152,9 @@ __device__ __forceinline__ void sublist_of(const LevelDev& lv, uint32_t cta, uin
     v = len > i0 ? (int)(len - i0 < lv.L ? len - i0 : lv.L) : 0;
 }
 
+#ifndef GBS_VEC_IO
+#define GBS_VEC_IO 1        // keys tiles: 16-byte global loads / stores (A/B switch)
+#endif
 #ifndef GBS_KEYS_CHAINS
 #define GBS_KEYS_CHAINS 1   // merge chains per thread (0 = automatic); 1 measured best at 1024x32
 #endif
@@ -246,21 +249,49 @@ struct Seg {
         }
     }
 
+    // Registers <- the tile's v items; returns the count the CTA sort is to treat as valid
+    // (items sit in a prefix of every warp span; sentinels elsewhere).  Keys load 16-byte
+    // vectors: the tile is read from the 16-byte boundary at or below its start, slot
+    // (j, c) of lane l in warp w holding position 128 j + 4 l + c + w 32 ITEMS - mis, so the
+    // first mis slots are sentinels and the sort sees v + mis slots (one vector per 4 keys;
+    // scalar loads only at the two ends).
     template <int M>
-    static __device__ __forceinline__ void load_regs(T (&x)[M], const void* src, const uint32_t* src_v,
-                                                     uint64_t off, int v, unsigned char* smem, int xf = 0)
+    static __device__ __forceinline__ int load_regs(T (&x)[M], const void* src, const uint32_t* src_v,
+                                                    uint64_t off, int v, unsigned char* smem, int xf = 0)
     {
         if constexpr (KIND == KIND_PAIRS) {
             load_keys(x, src, off, v, xf);
             load_vals(src_v, off, v, smem);
         } else if constexpr (KIND == KIND_KEYS) {
             const uint32_t* s = reinterpret_cast<const uint32_t*>(src) + off;
+            const int mis = (int)(((uintptr_t)s >> 2) & 3);
+            if (GBS_VEC_IO && ITEMS % 4 == 0 && v + mis <= TILE) {
+                const uint32_t* a = s - mis;                  // 16-byte aligned
+                const int q0 = (int)(threadIdx.x >> 5) * CS::WARP_SPAN + 4 * (int)(threadIdx.x & 31);
+#pragma unroll
+                for (int j = 0; j < ITEMS / 4; ++j) {
+                    const int q = q0 + 128 * j, p = q - mis;
+                    if (p >= 0 && p + 3 < v) {
+                        const uint4 u = __ldg(reinterpret_cast<const uint4*>(a + q));
+                        x[4 * j] = xf_in(u.x, xf);
+                        x[4 * j + 1] = xf_in(u.y, xf);
+                        x[4 * j + 2] = xf_in(u.z, xf);
+                        x[4 * j + 3] = xf_in(u.w, xf);
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < 4; ++c)
+                            x[4 * j + c] = (p + c >= 0 && p + c < v) ? xf_in(__ldg(a + q + c), xf) : CS::TMAX;
+                    }
+                }
+                return v + mis;
+            }
             const int p0 = CS::load_pos(0), rem = v - p0;     // load_pos(k) = p0 + 32k
 #pragma unroll
             for (int k = 0; k < ITEMS; ++k) x[k] = 32 * k < rem ? xf_in(s[p0 + 32 * k], xf) : CS::TMAX;
         } else {
             CS::load(x, reinterpret_cast<const KeyT*>(src) + off, v);
         }
+        return v;
     }
 
     // Fused Step 8+9: register slot k holds bucket position load_pos(k) (32 consecutive
@@ -316,7 +347,29 @@ struct Seg {
         const T* sm = reinterpret_cast<const T*>(smem);
         if constexpr (KIND == KIND_KEYS) {
             uint32_t* d = reinterpret_cast<uint32_t*>(dst) + dst_off;
-            if constexpr (BLOCK % (1 << CS::PAD) == 0) {
+            if (GBS_VEC_IO) {
+                // 16-byte stores: group g = positions 4g - mis .. 4g - mis + 3 lands on the
+                // g-th 16-byte word at or after the boundary below d (scalar at the ends);
+                // the four shared-memory reads of a group are conflict-free across a warp
+                const int mis = (int)(((uintptr_t)d >> 2) & 3);
+                uint32_t* a = d - mis;
+                const int ng = (v + mis + 3) >> 2;
+                for (int g = threadIdx.x; g < ng; g += BLOCK) {
+                    const int p = 4 * g - mis;
+                    if (p >= 0 && p + 3 < v) {
+                        uint4 u;
+                        u.x = xf_out((uint32_t)sm[CS::phys(p)], xf);
+                        u.y = xf_out((uint32_t)sm[CS::phys(p + 1)], xf);
+                        u.z = xf_out((uint32_t)sm[CS::phys(p + 2)], xf);
+                        u.w = xf_out((uint32_t)sm[CS::phys(p + 3)], xf);
+                        *reinterpret_cast<uint4*>(a + 4 * g) = u;
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < 4; ++c)
+                            if (p + c >= 0 && p + c < v) a[4 * g + c] = xf_out((uint32_t)sm[CS::phys(p + c)], xf);
+                    }
+                }
+            } else if constexpr (BLOCK % (1 << CS::PAD) == 0) {
                 // position tid + k BLOCK sits at phys(tid) + k (BLOCK + BLOCK >> PAD): one
                 // address, constant offsets (BLOCK is a multiple of the pad group)
                 const int t = threadIdx.x;
@@ -372,13 +425,13 @@ struct Adapt {
     using Sub = Adapt<KIND, BLOCK, (HALF ? ITEMS / 2 : ITEMS), (HALF ? DEPTH - 1 : 0)>;
 
     template <int M>
-    static __device__ __forceinline__ void load(T (&x)[M], const void* src, const uint32_t* src_v, uint64_t off,
-                                                int v, unsigned char* smem, int xf = 0)
+    static __device__ __forceinline__ int load(T (&x)[M], const void* src, const uint32_t* src_v, uint64_t off,
+                                               int v, unsigned char* smem, int xf = 0)
     {
         if constexpr (HALF) {
-            if (v <= S::TILE / 2) { Sub::load(x, src, src_v, off, v, smem, xf); return; }
+            if (v <= S::TILE / 2) return Sub::load(x, src, src_v, off, v, smem, xf);
         }
-        S::load_regs(x, src, src_v, off, v, smem, xf);
+        return S::load_regs(x, src, src_v, off, v, smem, xf);
     }
     template <int M>
     static __device__ __forceinline__ void sort(T (&x)[M], unsigned char* smem, int v)
@@ -418,8 +471,8 @@ struct Adapt {
             if (v <= S::TILE / 2) { Sub::run(src, src_v, off, v, dst, dst_v, smem, xf_i, xf_o); return; }
         }
         T x[ITEMS];
-        S::load_regs(x, src, src_v, off, v, smem, xf_i);
-        S::CS::sort(x, reinterpret_cast<T*>(smem), v);
+        const int vs = S::load_regs(x, src, src_v, off, v, smem, xf_i);
+        S::CS::sort(x, reinterpret_cast<T*>(smem), vs);
         S::store(dst, dst_v, off, v, smem, xf_o);
     }
 };
@@ -452,13 +505,18 @@ __global__ void __launch_bounds__(BLOCK, 1) k_local_sort(LevelDev lv)
     uint32_t tile = lv.tile_lo + blockIdx.x;
     uint64_t start = 0;
     int v = 0;
-    auto load_next = [&](uint64_t st, int vv) {   // into registers (pairs: the keys)
-        if constexpr (KIND == KIND_PAIRS) S::load_keys(x, lv.in, st, vv, lv.xf_in);
-        else S::load_regs(x, lv.in, lv.in_v, st, vv, smem_raw, lv.xf_in);
+    auto load_next = [&](uint64_t st, int vv) -> int {   // into registers (pairs: the keys)
+        if constexpr (KIND == KIND_PAIRS) {
+            S::load_keys(x, lv.in, st, vv, lv.xf_in);
+            return vv;
+        } else {
+            return S::load_regs(x, lv.in, lv.in_v, st, vv, smem_raw, lv.xf_in);
+        }
     };
+    int vs = 0;                      // the count the CTA sort treats as valid (load_regs)
     if (tile < ntiles) {
         sublist_of(lv, tile, start, v);
-        if (pipe) load_next(start, v);
+        if (pipe) vs = load_next(start, v);
     }
     for (; tile < ntiles; tile += gridDim.x) {
         const uint32_t b = tile / lv.m, i = tile % lv.m;
@@ -481,10 +539,11 @@ __global__ void __launch_bounds__(BLOCK, 1) k_local_sort(LevelDev lv)
                                           (int)lv.presorted);
             } else {
                 if constexpr (KIND == KIND_PAIRS) S::load_vals(lv.in_v, start, v, smem_raw);
-                S::CS::sort(x, sm, v);
+                S::CS::sort(x, sm, vs);
             }
         }
-        if (pipe && nv > 0) load_next(nstart, nv);   // in flight during the store
+        int nvs = 0;
+        if (pipe && nv > 0) nvs = load_next(nstart, nv);   // in flight during the store
         if (v > 0) S::store(lv.srt, lv.srt_v, start, v, smem_raw);
         u64* smp = lv.samples + ((uint64_t)b * lv.m + i) * lv.s;
         for (uint32_t k = threadIdx.x; k < lv.s; k += BLOCK) {
@@ -504,6 +563,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_local_sort(LevelDev lv)
         __syncthreads();                     // shared memory is reused by the next sublist
         start = nstart;
         v = nv;
+        vs = nvs;
     }
 }
 
@@ -547,8 +607,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BLOCK, 1) k_local_so
             const int nr = max(0, min(nv - rank * H, H));
             if (nr > 0) prefetch_l2(reinterpret_cast<const T*>(lv.in) + ns + (uint64_t)rank * H, (size_t)nr * 4);
         }
-        S::load_regs(x, lv.in, nullptr, start + (uint64_t)rank * H, vr, smem_raw, lv.xf_in);
-        CS::sort(x, sm, vr);                            // positions >= vr read as TMAX
+        const int vs = S::load_regs(x, lv.in, nullptr, start + (uint64_t)rank * H, vr, smem_raw, lv.xf_in);
+        CS::sort(x, sm, vs);                            // positions >= vr read as TMAX
         cluster.sync();                                 // both halves sorted and visible
         const T* peer = cluster.map_shared_rank(sm, rank ^ 1);
         if (threadIdx.x < 32) {
@@ -1569,8 +1629,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(BLOCK, 1) k_segment_
             const int nr = max(0, min(nv - rank * H, H));
             if (nr > 0) prefetch_l2(reinterpret_cast<const T*>(lv.reloc) + no + (uint64_t)rank * H, (size_t)nr * 4);
         }
-        S::load_regs(x, lv.reloc, nullptr, off + (uint64_t)rank * H, vr, smem_raw);
-        CS::sort(x, sm, vr);
+        const int vs = S::load_regs(x, lv.reloc, nullptr, off + (uint64_t)rank * H, vr, smem_raw);
+        CS::sort(x, sm, vs);
         cluster.sync();                                 // both halves sorted and visible
         const T* peer = cluster.map_shared_rank(sm, rank ^ 1);
         if (threadIdx.x < 32) {                         // a* = merge-path split of diagonal H

@@ -8,7 +8,10 @@ is present, every call raises.
     import paper_1002_4464_b200 as gbs
     gbs.sort_keys(t)              # t: CUDA int32/uint32 tensor, sorted in place (unsigned)
     gbs.sort_pairs(k, v)          # stable by key, in place
-    out = gbs.sort_keys_dist(t)   # one process per GPU (torch.distributed initialised)
+    gbs.sort_keys_typed(f)        # int32 / float32 keys by value (floats: IEEE-754 totalOrder)
+    gbs.sort_keys64(x)            # uint64 / int64 / float64 keys; sort_pairs64(k, v) with values
+    gbs.sort_pairs_host(hk, hv, dk, dv)   # pinned host buffers in and out (copies inside)
+    part = gbs.sort_keys_dist(t, gbs.Comm())   # one process per GPU (torch.distributed up)
 """
 from __future__ import annotations
 

@@ -139,6 +139,7 @@ struct Node {
     int step4 = -1, step9 = -1;
     size_t o_samples = 0, o_splitters = 0, o_a = 0, o_l = 0, o_state = 0;
     size_t o_child_off = 0, o_child_len = 0, o_reloc = SIZE_MAX, o_reloc_v = SIZE_MAX;
+    size_t o_child_scnt = 0;   // the nested level's samples to sort per problem (k_child_desc)
     size_t o_tiers = 0;   // Step 9 size-tier lists (3 x B*s) + counters (4)
     size_t o_pex = 0;     // fused Step 8+9: run starts P_i,j-1 (B*m*s)
     bool fuse89 = false;  // Step 9 gathers straight from the sorted sublists (no Step 8 pass)
@@ -379,6 +380,7 @@ static int build_node(Plan& P, int kind, uint32_t B, uint64_t N, uint32_t pad_ba
     } else {
         P.nodes[idx].o_child_off = P.alloc((uint64_t)B * s * 8);
         P.nodes[idx].o_child_len = P.alloc((uint64_t)B * s * 4);
+        P.nodes[idx].o_child_scnt = P.alloc((uint64_t)B * s * 4);
         P.launches += reloc_launches(kind) + 1;  // relocate + child descriptors
         const uint64_t nb = (uint64_t)B * s;
         if (nb >= (1ull << 31)) { snprintf(g_err, sizeof g_err, "too many nested problems"); return -1; }
@@ -700,6 +702,8 @@ struct Bufs {
     void* srt = nullptr;
     // typed keys: transform at the first level's loads / the last level's stores
     int xf_in = 0, xf_out = 0;
+    // nested level: per problem, the samples of its non-empty sublists (Step 4 sorts these)
+    const uint32_t* scnt = nullptr;
 };
 
 template <int KIND>
@@ -985,7 +989,9 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
         const Node& c = P.nodes[nd.step4];
         Bufs b4{lv.samples, c.leaf ? (void*)lv.samples : (void*)(ws + c.o_reloc), lv.samples, nullptr, nullptr, nullptr};
         // each sublist's s samples are sorted and contiguous: runs of length s
-        Probs p4{nullptr, nullptr, (uint64_t)nd.m * nd.s, nd.m * nd.s, nd.s};
+        // (a nested level sorts only the samples of each problem's non-empty sublists: the
+        // rest are virtual sentinels already in their sorted places, k_child_desc)
+        Probs p4{nullptr, bf.scnt, (uint64_t)nd.m * nd.s, nd.m * nd.s, nd.s};
         gbs_status_t r = exec(P, nd.step4, ws, b4, p4, st, 0);
         if (r) return r;
     }
@@ -1093,12 +1099,15 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
         lv.child_off = reinterpret_cast<u64*>(ws + nd.o_child_off);
         lv.child_len = reinterpret_cast<uint32_t*>(ws + nd.o_child_len);
         const uint64_t tot = (uint64_t)nd.B * nd.s;
-        launch_k(k_child_desc, (unsigned)((tot + 255) / 256), 256, 0, st, lv);
+        const Node& ch = P.nodes[nd.step9];
+        uint32_t* scnt = (!ch.leaf && ch.step4 >= 0) ? reinterpret_cast<uint32_t*>(ws + nd.o_child_scnt) : nullptr;
+        launch_k(k_child_desc, (unsigned)((tot + 255) / 256), 256, 0, st, lv, scnt, ch.L, ch.s);
         GBS_LAUNCHED();
         // the nested level sorts its problems in place in the reloc buffer and uses the
         // sublists' buffer (dead after Step 8) as its own relocation target
         Bufs b9{bf.reloc, bf.srt ? bf.srt : bf.in, bf.out, bf.reloc_v, bf.in_v, bf.out_v};
         b9.xf_out = bf.xf_out;   // the keys entered the sort at this level's Step 2
+        b9.scnt = scnt;
         Probs p9{lv.child_off, lv.child_len, 0, 0};
         gbs_status_t r = exec(P, nd.step9, ws, b9, p9, st, 0);
         if (r) return r;

@@ -1753,8 +1753,12 @@ __global__ void k_check_level(LevelDev lv, unsigned* flag, int only_splitters)
     }
 }
 
-// Nested Step 9: the buckets of this level become the problems of the next level.
-__global__ void k_child_desc(LevelDev lv)
+// Nested Step 9: the buckets of this level become the problems of the next level.  Also
+// the number of samples the next level's Step 4 must sort per problem: those of its
+// non-empty sublists, ceil(len / Lc) * sc.  The samples of empty sublists are virtual
+// sentinels (key 0xFFFFFFFF, tags above every real item, R8), already in sorted order
+// after every real sample, so they stay where they are.
+__global__ void k_child_desc(LevelDev lv, uint32_t* child_scnt, uint32_t Lc, uint32_t sc)
 {
     pdl_entry();
     const uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1765,6 +1769,7 @@ __global__ void k_child_desc(LevelDev lv)
     const uint32_t en = j + 1 < lv.s ? l0[j + 1] : lv.pr.length(b);
     lv.child_off[idx] = lv.pr.offset(b) + st;
     lv.child_len[idx] = en - st;
+    if (child_scnt) child_scnt[idx] = (uint32_t)(((uint64_t)(en - st) + Lc - 1) / Lc * sc);
 }
 
 }  // namespace gbs

@@ -947,6 +947,10 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
         pm.ev = g_prof_calls.back().ev.data();
         pm.st = st;
     }
+    // zero Step 7's look-back words and its longest-run word before the level's first
+    // kernel, where the memset delays nothing (between Steps 6 and 7 it would)
+    const unsigned nblk = (nd.s + 31) / 32;
+    GBS_CUDA(cudaMemsetAsync(lv.state, 0, (size_t)nd.B * nblk * 8 + 8, st));
     pm.mark();
 
     // Steps 2-3: local sort + local samples (one CTA per sublist)
@@ -1030,9 +1034,7 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
     pm.mark();
 
     // Step 7: column-major exclusive scan -> l
-    const unsigned nblk = (nd.s + 31) / 32;
     lv.maxrun = reinterpret_cast<uint32_t*>(lv.state + (size_t)nd.B * nblk);   // one word past the look-back words
-    GBS_CUDA(cudaMemsetAsync(lv.state, 0, (size_t)nd.B * nblk * 8 + 8, st));
     launch_k(k_scan, nd.B * nblk, SCAN_BLOCK, 0, st, lv);
     GBS_LAUNCHED();
     if (stop == 7) return GBS_SUCCESS;

@@ -198,55 +198,25 @@ __device__ __forceinline__ uint32_t xf_out(uint32_t x, int xf) { return xf ? key
 
 // ------------------------------------------------------------------ segment I/O
 // One tile of `v` items at element offset `off` of an HBM buffer: registers <- HBM
-// (load_regs), on-chip sort (CS::sort, result in shared memory), HBM <- shared memory
-// (store).  Pairs sort (key << 32 | position) and stage the values in vsm.
+// (load_regs), on-chip sort (sort: CS::sort, result in shared memory), HBM <- shared
+// memory (store).  Keys and u64 composites; pairs are the specialisation below.
 template <int KIND, int BLOCK, int ITEMS>
 struct Seg {
     using T = typename ItemT<KIND>::T;
     using CS = CtaSort<T, BLOCK, ITEMS, (KIND == KIND_KEYS ? GBS_KEYS_CHAINS : GBS_WIDE_CHAINS)>;
     using KeyT = typename std::conditional<KIND == KIND_U64, unsigned long long, uint32_t>::type;  // in HBM
     static constexpr int TILE = CS::TILE;
-    __host__ __device__ static constexpr size_t smem_bytes()
-    {
-        return sizeof(T) * CS::SMEM_ELEMS + (KIND == KIND_PAIRS ? sizeof(uint32_t) * TILE : 0);
-    }
-    static __device__ __forceinline__ uint32_t* vsm_of(unsigned char* smem)
-    {
-        return reinterpret_cast<uint32_t*>(reinterpret_cast<T*>(smem) + CS::SMEM_ELEMS);
-    }
+    __host__ __device__ static constexpr size_t smem_bytes() { return sizeof(T) * CS::SMEM_ELEMS; }
 
-    // Pairs: the keys of positions load_pos(k) as (key << 32 | position) composites (stable:
-    // ties by position) ...
     template <int M>
-    static __device__ __forceinline__ void load_keys(T (&x)[M], const void* src, uint64_t off, int v, int xf = 0)
+    static __device__ __forceinline__ void sort(T (&x)[M], unsigned char* smem, int v)
     {
-        static_assert(KIND == KIND_PAIRS, "pairs only");
-        const int p0 = CS::load_pos(0), rem = v - p0;
-        const uint32_t* s = reinterpret_cast<const uint32_t*>(src) + off + p0;
-#pragma unroll
-        for (int k = 0; k < ITEMS; ++k) {
-            const uint32_t key = 32 * k < rem ? xf_in(__ldg(s + 32 * k), xf) : 0xFFFFFFFFu;
-            x[k] = ((T)key << 32) | (T)(uint32_t)(p0 + 32 * k);
-        }
+        CS::sort(x, reinterpret_cast<T*>(smem), v);
     }
-    // ... and their values parked in shared memory at their positions (gathered by position
-    // at the write-back): every load of the thread in flight before the stores
-    static __device__ __forceinline__ void load_vals(const uint32_t* src_v, uint64_t off, int v, unsigned char* smem)
+    // sorted item r (keys: the key; u64: the composite) after sort()
+    static __device__ __forceinline__ T item_at(const unsigned char* smem, int r)
     {
-        uint32_t* vsm = vsm_of(smem);
-        const uint32_t* sv = src_v + off;
-        constexpr int PER = (TILE + BLOCK - 1) / BLOCK;
-        uint32_t t[PER];
-#pragma unroll
-        for (int k = 0; k < PER; ++k) {
-            const int p = (int)threadIdx.x + k * BLOCK;
-            t[k] = p < v ? __ldg(sv + p) : 0u;
-        }
-#pragma unroll
-        for (int k = 0; k < PER; ++k) {
-            const int p = (int)threadIdx.x + k * BLOCK;
-            if (p < v) vsm[p] = t[k];
-        }
+        return reinterpret_cast<const T*>(smem)[CS::phys(r)];
     }
 
     // Registers <- the tile's v items; returns the count the CTA sort is to treat as valid
@@ -259,10 +229,7 @@ struct Seg {
     static __device__ __forceinline__ int load_regs(T (&x)[M], const void* src, const uint32_t* src_v,
                                                     uint64_t off, int v, unsigned char* smem, int xf = 0)
     {
-        if constexpr (KIND == KIND_PAIRS) {
-            load_keys(x, src, off, v, xf);
-            load_vals(src_v, off, v, smem);
-        } else if constexpr (KIND == KIND_KEYS) {
+        if constexpr (KIND == KIND_KEYS) {
             const uint32_t* s = reinterpret_cast<const uint32_t*>(src) + off;
             const int mis = (int)(((uintptr_t)s >> 2) & 3);
             if (GBS_VEC_IO && ITEMS % 4 == 0 && v + mis <= TILE) {
@@ -298,8 +265,6 @@ struct Seg {
     // positions per warp instruction, as for a relocated bucket, so the reads stay
     // coalesced inside each run).  Each lane finds the run of its first position by
     // binary search over the run table, then walks forward (positions only grow).
-    // Pairs carry the position p as the tie-break and park the value in vsm[p], exactly
-    // as load_regs does for a relocated bucket.
     template <int M, typename G>
     static __device__ __forceinline__ void load_gather(T (&x)[M], const G& g, int v, unsigned char* smem)
     {
@@ -316,7 +281,6 @@ struct Seg {
         }
         uint32_t base = g.run[i].y;
         uint2 nx = g.run[i + 1];
-        uint32_t* vsm = KIND == KIND_PAIRS ? vsm_of(smem) : nullptr;
 #pragma unroll
         for (int k = 0; k < ITEMS; ++k) {
             const int p = pbase + 32 * k;
@@ -327,16 +291,9 @@ struct Seg {
                     nx = g.run[i + 1];
                 }
                 const uint32_t q = base + (uint32_t)p;
-                if constexpr (KIND == KIND_PAIRS) {
-                    const uint32_t key = __ldg(reinterpret_cast<const uint32_t*>(g.src) + q);
-                    x[k] = ((T)key << 32) | (T)(uint32_t)p;
-                    vsm[p] = __ldg(g.src_v + q);
-                } else {
-                    x[k] = (T)__ldg(reinterpret_cast<const KeyT*>(g.src) + q);
-                }
+                x[k] = (T)__ldg(reinterpret_cast<const KeyT*>(g.src) + q);
             } else {
-                if constexpr (KIND == KIND_PAIRS) x[k] = ((T)0xFFFFFFFFu << 32) | (T)(uint32_t)p;
-                else x[k] = CS::TMAX;
+                x[k] = CS::TMAX;
             }
         }
     }
@@ -381,18 +338,301 @@ struct Seg {
             } else {
                 for (int p = threadIdx.x; p < v; p += BLOCK) d[p] = xf_out((uint32_t)sm[CS::phys(p)], xf);
             }
-        } else if constexpr (KIND == KIND_PAIRS) {
-            const uint32_t* vsm = vsm_of(smem);
-            uint32_t* d = reinterpret_cast<uint32_t*>(dst) + dst_off;
-            uint32_t* dv = dst_v + dst_off;
-            for (int p = threadIdx.x; p < v; p += BLOCK) {
-                const T c = sm[CS::phys(p)];
-                d[p] = xf_out((uint32_t)(c >> 32), xf);
-                dv[p] = vsm[(uint32_t)c];
-            }
         } else {
             unsigned long long* d = reinterpret_cast<unsigned long long*>(dst) + dst_off;
             for (int p = threadIdx.x; p < v; p += BLOCK) d[p] = sm[CS::phys(p)];
+        }
+    }
+};
+
+// Pairs (u32 key -> u32 value, stable by key; R7).  Sorting (key << 32 | position)
+// composites moves 8 bytes per item through every shared-memory merge level; the tile
+// instead sorts 4-byte packed items P = (prefix << POSB) | position, prefix = the top
+// 32 - POSB bits of key - min (the tile's key range shifted into 32 - POSB bits), on the
+// keys' CtaSort, then restores the exact order (key, position):
+//   - prefix is monotone in key, so only items of equal prefix can be out of key order,
+//     and inside such a group the sort left them in position order;
+//   - with the keys gathered by position, odd-even transposition sort restricted to
+//     neighbours of equal prefix (swap iff the later key is strictly smaller) sorts every
+//     group by key with equal keys kept in position order -- the stable order.  It stops
+//     after the first round pair with no swap (one round pair when the keys never
+//     collide in their prefix: a key range below 2^(32-POSB), equal keys, presorted runs).
+// Uniform keys over a tile of 2^14 give groups of 1-4 items (2-3 round pairs).  A tile
+// whose groups need more than PK_MAX_ITERS round pairs (a long unsorted run of keys
+// sharing a prefix) is sorted as (key << 32 | position) composites instead, in the same
+// shared memory: the result is identical either way (the stable sort), only the cost
+// differs.  Values are parked at their positions and gathered at the write-back.
+#ifndef GBS_PK_MAX_ITERS
+#define GBS_PK_MAX_ITERS 16
+#endif
+template <int BLOCK, int ITEMS>
+struct Seg<KIND_PAIRS, BLOCK, ITEMS> {
+    using T = uint32_t;                                   // register items: keys, then P
+    using KeyT = uint32_t;                                // in HBM
+    using CS = CtaSort<uint32_t, BLOCK, ITEMS, GBS_KEYS_CHAINS>;
+    using CS64 = CtaSort<unsigned long long, BLOCK, ITEMS, GBS_WIDE_CHAINS>;   // fallback
+    static constexpr int TILE = CS::TILE;
+    static constexpr int NW = BLOCK / 32;
+    static constexpr int POSB = Log2<TILE>::value + ((TILE & (TILE - 1)) ? 1 : 0);   // position bits
+    static constexpr uint32_t PMASK = (1u << POSB) - 1;
+    static_assert(POSB <= 16 && ITEMS % 2 == 0 && BLOCK % 32 == 0, "packed pairs tile");
+    static_assert(CS::SMEM_ELEMS == CS64::SMEM_ELEMS, "one padded layout for both sorts");
+    struct Ctrl {
+        uint32_t mn[NW], mx[NW];          // key range reduction
+        uint32_t fP[NW], fK[NW], lP[NW], lK[NW];   // first / last item of every warp
+        int fb;                           // 1: the tile was sorted as composites
+    };
+    // shared memory: [ psm u32 | ksm u32 ] (or the fallback's u64 array) | vsm u32 | Ctrl
+    __host__ __device__ static constexpr size_t region_bytes() { return 8 * (size_t)CS::SMEM_ELEMS; }
+    __host__ __device__ static constexpr size_t smem_bytes()
+    {
+        return region_bytes() + 4 * (size_t)TILE + sizeof(Ctrl);
+    }
+    static __device__ __forceinline__ uint32_t* psm_of(unsigned char* smem) { return reinterpret_cast<uint32_t*>(smem); }
+    static __device__ __forceinline__ uint32_t* ksm_of(unsigned char* smem)
+    {
+        return reinterpret_cast<uint32_t*>(smem) + CS::SMEM_ELEMS;
+    }
+    static __device__ __forceinline__ uint32_t* vsm_of(unsigned char* smem)
+    {
+        return reinterpret_cast<uint32_t*>(smem + region_bytes());
+    }
+    static __device__ __forceinline__ Ctrl* ctrl_of(unsigned char* smem)
+    {
+        return reinterpret_cast<Ctrl*>(smem + region_bytes() + 4 * (size_t)TILE);
+    }
+
+    // the keys of positions load_pos(k) (0xFFFFFFFF beyond v; registers only, so it may
+    // run while the previous tile is written back)
+    template <int M>
+    static __device__ __forceinline__ void load_keys(uint32_t (&x)[M], const void* src, uint64_t off, int v, int xf = 0)
+    {
+        const int p0 = CS::load_pos(0), rem = v - p0;
+        const uint32_t* s = reinterpret_cast<const uint32_t*>(src) + off + p0;
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k) x[k] = 32 * k < rem ? xf_in(__ldg(s + 32 * k), xf) : 0xFFFFFFFFu;
+    }
+    // the values parked in shared memory at their positions: every load of the thread in
+    // flight before the stores
+    static __device__ __forceinline__ void load_vals(const uint32_t* src_v, uint64_t off, int v, unsigned char* smem)
+    {
+        uint32_t* vsm = vsm_of(smem);
+        const uint32_t* sv = src_v + off;
+        constexpr int PER = (TILE + BLOCK - 1) / BLOCK;
+        uint32_t t[PER];
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int p = (int)threadIdx.x + k * BLOCK;
+            t[k] = p < v ? __ldg(sv + p) : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int p = (int)threadIdx.x + k * BLOCK;
+            if (p < v) vsm[p] = t[k];
+        }
+    }
+    template <int M>
+    static __device__ __forceinline__ int load_regs(uint32_t (&x)[M], const void* src, const uint32_t* src_v,
+                                                    uint64_t off, int v, unsigned char* smem, int xf = 0)
+    {
+        load_keys(x, src, off, v, xf);
+        load_vals(src_v, off, v, smem);
+        return v;
+    }
+    // fused Step 8+9: bucket position load_pos(k) gathered through the run table (see the
+    // primary template); the value parked at its position
+    template <int M, typename G>
+    static __device__ __forceinline__ void load_gather(uint32_t (&x)[M], const G& g, int v, unsigned char* smem)
+    {
+        const int pbase = CS::load_pos(0);
+        int i = 0;
+        if (pbase < v) {
+            int lo = 0, hi = g.m - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if ((int)g.run[mid].x <= pbase) lo = mid;
+                else hi = mid - 1;
+            }
+            i = lo;
+        }
+        uint32_t base = g.run[i].y;
+        uint2 nx = g.run[i + 1];
+        uint32_t* vsm = vsm_of(smem);
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k) {
+            const int p = pbase + 32 * k;
+            if (p < v) {
+                while (p >= (int)nx.x) {
+                    base = nx.y;
+                    ++i;
+                    nx = g.run[i + 1];
+                }
+                const uint32_t q = base + (uint32_t)p;
+                x[k] = __ldg(reinterpret_cast<const uint32_t*>(g.src) + q);
+                vsm[p] = __ldg(g.src_v + q);
+            } else {
+                x[k] = 0xFFFFFFFFu;
+            }
+        }
+    }
+
+    // compare-exchange of neighbours a (earlier) and b inside one prefix group
+    static __device__ __forceinline__ void cx(bool eq, uint32_t& pa, uint32_t& ka, uint32_t& pb, uint32_t& kb, bool& sw)
+    {
+        const bool s = eq && kb < ka;
+        const uint32_t p0 = s ? pb : pa, p1 = s ? pa : pb, k0 = s ? kb : ka, k1 = s ? ka : kb;
+        pa = p0; pb = p1; ka = k0; kb = k1;
+        sw |= s;
+    }
+
+    // x[k] = the key of position load_pos(k) (0xFFFFFFFF beyond v).  On return the
+    // tile's stable order is in shared memory (key_at / store).  Block-synchronised.
+    template <int M>
+    static __device__ __forceinline__ void sort(uint32_t (&x)[M], unsigned char* smem, int v)
+    {
+        uint32_t* psm = psm_of(smem);
+        uint32_t* ksm = ksm_of(smem);
+        Ctrl* c = ctrl_of(smem);
+        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+        const int p0 = CS::load_pos(0);
+        // keys parked at their positions; the tile's key range
+        uint32_t lo = 0xFFFFFFFFu, hi = 0;
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k) {
+            if (p0 + 32 * k < v) {
+                ksm[CS::phys(p0 + 32 * k)] = x[k];
+                lo = min(lo, x[k]);
+                hi = max(hi, x[k]);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        }
+        if (lane == 0) {
+            c->mn[w] = lo;
+            c->mx[w] = hi;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < NW; ++q) {
+            lo = min(lo, c->mn[q]);
+            hi = max(hi, c->mx[q]);
+        }
+        const int bits = hi > lo ? 32 - __clz((int)(hi - lo)) : 0;
+        const int shift = max(0, bits - (32 - POSB));
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k) {
+            const int p = p0 + 32 * k;
+            x[k] = p < v ? (((x[k] - lo) >> shift) << POSB) | (uint32_t)p : 0xFFFFFFFFu;
+        }
+        CS::sort(x, psm, v);     // x: the thread's sorted outputs [start, start + ITEMS)
+
+        // exact order inside prefix groups: odd-even transposition on (prefix, key)
+        const int start = threadIdx.x * ITEMS;
+        uint32_t K[ITEMS];
+        uint32_t eqm = 0;        // bit i: items i and i+1 share a prefix (invariant under swaps)
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) K[i] = start + i < v ? ksm[CS::phys(x[i] & PMASK)] : 0xFFFFFFFFu;
+#pragma unroll
+        for (int i = 0; i + 1 < ITEMS; ++i) eqm |= ((x[i] >> POSB) == (x[i + 1] >> POSB) ? 1u : 0u) << i;
+        int iter = 0, fb = 0;
+        for (;;) {
+            bool sw = false;
+            if (eqm) {
+#pragma unroll
+                for (int i = 0; i + 1 < ITEMS; i += 2) cx((eqm >> i) & 1, x[i], K[i], x[i + 1], K[i + 1], sw);
+#pragma unroll
+                for (int i = 1; i + 1 < ITEMS; i += 2) cx((eqm >> i) & 1, x[i], K[i], x[i + 1], K[i + 1], sw);
+            }
+            // odd pair across threads: (last of t, first of t + 1)
+            uint32_t fP = __shfl_down_sync(0xffffffffu, x[0], 1), fK = __shfl_down_sync(0xffffffffu, K[0], 1);
+            uint32_t lP = __shfl_up_sync(0xffffffffu, x[ITEMS - 1], 1), lK = __shfl_up_sync(0xffffffffu, K[ITEMS - 1], 1);
+            if (lane == 0) {
+                c->fP[w] = x[0];
+                c->fK[w] = K[0];
+            }
+            if (lane == 31) {
+                c->lP[w] = x[ITEMS - 1];
+                c->lK[w] = K[ITEMS - 1];
+            }
+            __syncthreads();
+            const bool has_next = threadIdx.x + 1 < BLOCK, has_prev = threadIdx.x > 0;
+            if (lane == 31 && has_next) {
+                fP = c->fP[w + 1];
+                fK = c->fK[w + 1];
+            }
+            if (lane == 0 && has_prev) {
+                lP = c->lP[w - 1];
+                lK = c->lK[w - 1];
+            }
+            if (has_next && (x[ITEMS - 1] >> POSB) == (fP >> POSB) && fK < K[ITEMS - 1]) {
+                x[ITEMS - 1] = fP;
+                K[ITEMS - 1] = fK;
+                sw = true;
+            }
+            if (has_prev && (lP >> POSB) == (x[0] >> POSB) && K[0] < lK) {
+                x[0] = lP;
+                K[0] = lK;
+                sw = true;
+            }
+            if (!__syncthreads_or(sw)) break;
+            if (++iter == GBS_PK_MAX_ITERS) {
+                fb = 1;
+                break;
+            }
+        }
+        if (threadIdx.x == 0) c->fb = fb;
+        if (!fb) {
+            // every gather is done (the loop ends on a barrier): sorted keys and P in place
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i) {
+                ksm[CS::phys(start + i)] = K[i];
+                psm[CS::phys(start + i)] = x[i];
+            }
+            __syncthreads();
+            return;
+        }
+        // fallback: the stable sort of (key << 32 | position) composites
+        unsigned long long xx[ITEMS];
+#pragma unroll
+        for (int k = 0; k < ITEMS; ++k) {
+            const int p = p0 + 32 * k;
+            xx[k] = p < v ? ((unsigned long long)ksm[CS::phys(p)] << 32) | (unsigned)p : ~0ull;
+        }
+        __syncthreads();         // ksm read before the composites overwrite it
+        CS64::sort(xx, reinterpret_cast<unsigned long long*>(smem), v);
+    }
+
+    // key of sorted item r (after sort)
+    static __device__ __forceinline__ uint32_t key_at(unsigned char* smem, int r)
+    {
+        if (ctrl_of(smem)->fb) return (uint32_t)(reinterpret_cast<const unsigned long long*>(smem)[CS::phys(r)] >> 32);
+        return ksm_of(smem)[CS::phys(r)];
+    }
+    static __device__ __forceinline__ uint32_t item_at(unsigned char* smem, int r) { return key_at(smem, r); }
+
+    static __device__ __forceinline__ void store(void* dst, uint32_t* dst_v, uint64_t dst_off, int v,
+                                                 unsigned char* smem, int xf = 0)
+    {
+        const uint32_t* vsm = vsm_of(smem);
+        uint32_t* d = reinterpret_cast<uint32_t*>(dst) + dst_off;
+        uint32_t* dv = dst_v + dst_off;
+        if (ctrl_of(smem)->fb) {
+            const unsigned long long* sm = reinterpret_cast<const unsigned long long*>(smem);
+            for (int p = threadIdx.x; p < v; p += BLOCK) {
+                const unsigned long long cc = sm[CS::phys(p)];
+                d[p] = xf_out((uint32_t)(cc >> 32), xf);
+                dv[p] = vsm[(uint32_t)cc];
+            }
+            return;
+        }
+        const uint32_t* psm = psm_of(smem);
+        const uint32_t* ksm = ksm_of(smem);
+        for (int p = threadIdx.x; p < v; p += BLOCK) {
+            d[p] = xf_out(ksm[CS::phys(p)], xf);
+            dv[p] = vsm[psm[CS::phys(p)] & PMASK];
         }
     }
 };
@@ -439,7 +679,7 @@ struct Adapt {
         if constexpr (HALF) {
             if (v <= S::TILE / 2) { Sub::sort(x, smem, v); return; }
         }
-        S::CS::sort(x, reinterpret_cast<T*>(smem), v);
+        S::sort(x, smem, v);
     }
     static __device__ __forceinline__ void store(void* dst, uint32_t* dst_v, uint64_t off, int v, unsigned char* smem,
                                                  int xf = 0)
@@ -459,7 +699,7 @@ struct Adapt {
         }
         T x[ITEMS];
         S::load_gather(x, g, v, smem);
-        S::CS::sort(x, reinterpret_cast<T*>(smem), v);
+        S::sort(x, smem, v);
         S::store(dst, dst_v, off, v, smem, xf_o);
     }
     // load + sort + store with a register array sized for the chosen tile
@@ -472,7 +712,7 @@ struct Adapt {
         }
         T x[ITEMS];
         const int vs = S::load_regs(x, src, src_v, off, v, smem, xf_i);
-        S::CS::sort(x, reinterpret_cast<T*>(smem), vs);
+        S::sort(x, smem, vs);
         S::store(dst, dst_v, off, v, smem, xf_o);
     }
 };
@@ -539,7 +779,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_local_sort(LevelDev lv)
                                           (int)lv.presorted);
             } else {
                 if constexpr (KIND == KIND_PAIRS) S::load_vals(lv.in_v, start, v, smem_raw);
-                S::CS::sort(x, sm, vs);
+                S::sort(x, smem_raw, vs);
             }
         }
         int nvs = 0;
@@ -554,8 +794,7 @@ __global__ void __launch_bounds__(BLOCK, 1) k_local_sort(LevelDev lv)
                 c = (int)r < v ? (unsigned long long)sm[S::CS::phys(r)] : pad64(lv.pad_base, i0 + r - len);
             } else {
                 uint32_t key = 0xFFFFFFFFu;
-                if ((int)r < v) key = KIND == KIND_KEYS ? (uint32_t)sm[S::CS::phys(r)]
-                                                        : (uint32_t)((unsigned long long)sm[S::CS::phys(r)] >> 32);
+                if ((int)r < v) key = (uint32_t)S::item_at(smem_raw, (int)r);
                 c = ((unsigned long long)key << 32) | tag;
             }
             smp[k] = c;

@@ -32,6 +32,7 @@ def test_graph_capture_and_replay(dev, n, pairs):
     s = torch.cuda.Stream(dev)
     # warm-up outside the capture (one-time kernel attribute setup, side streams)
     keys.copy_(gi.generate_torch("uniform", n, seed=1, device=dev))
+    s.wait_stream(torch.cuda.current_stream(dev))   # the input is written on the current stream
     with torch.cuda.stream(s):
         if pairs:
             vals.copy_(torch.arange(n, dtype=torch.int32, device=dev))

@@ -161,6 +161,23 @@ struct Node {
 #endif
 #define GBS_BIG_KEYS GBS_KEYS_BLOCK, GBS_KEYS_ITEMS
 #define GBS_BIG_WIDE GBS_WIDE_BLOCK, GBS_WIDE_ITEMS
+// Step 9 of pairs (packed 4-byte tile items): the full tile, the mid tier and the tier of
+// buckets up to its capacity (tier 0)
+#ifndef GBS_PAIRS_BIG_BLOCK
+#define GBS_PAIRS_BIG_BLOCK 1024
+#define GBS_PAIRS_BIG_ITEMS 16
+#endif
+#ifndef GBS_PAIRS_MID_BLOCK
+#define GBS_PAIRS_MID_BLOCK 1024
+#define GBS_PAIRS_MID_ITEMS 10
+#endif
+#ifndef GBS_PAIRS_T0_BLOCK
+#define GBS_PAIRS_T0_BLOCK 512
+#define GBS_PAIRS_T0_ITEMS 16
+#endif
+// the full-tile CTA of Step 9 per kind
+#define BIGB(K) ((K) == KIND_KEYS ? GBS_KEYS_BLOCK : ((K) == KIND_PAIRS ? GBS_PAIRS_BIG_BLOCK : GBS_WIDE_BLOCK))
+#define BIGI(K) ((K) == KIND_KEYS ? GBS_KEYS_ITEMS : ((K) == KIND_PAIRS ? GBS_PAIRS_BIG_ITEMS : GBS_WIDE_ITEMS))
 #ifndef GBS_PAIRS_LOCAL_BLOCK
 #define GBS_PAIRS_LOCAL_BLOCK 512   // Step 2 of pairs: 512 x 32 (C4 80.9 -> 78.8 ms vs 1024 x 16)
 #define GBS_PAIRS_LOCAL_ITEMS 32
@@ -189,10 +206,12 @@ struct Node {
 #ifndef GBS_MID_KEYS_ITEMS_NESTED
 #define GBS_MID_KEYS_ITEMS_NESTED 40
 #endif
-#define MID_BLOCK_OF(KIND) ((KIND) == KIND_KEYS ? GBS_MID_TOP_BLOCK : 1024)
-#define MID_ITEMS_OF(KIND) ((KIND) == KIND_KEYS ? GBS_MID_TOP_ITEMS : GBS_WIDE_ITEMS * 5 / 8)
+#define MID_BLOCK_OF(KIND) ((KIND) == KIND_KEYS ? GBS_MID_TOP_BLOCK : ((KIND) == KIND_PAIRS ? GBS_PAIRS_MID_BLOCK : 1024))
+#define MID_ITEMS_OF(KIND) \
+    ((KIND) == KIND_KEYS ? GBS_MID_TOP_ITEMS : ((KIND) == KIND_PAIRS ? GBS_PAIRS_MID_ITEMS : GBS_WIDE_ITEMS * 5 / 8))
 static uint32_t mid_cap(int kind, uint32_t B)
 {
+    if (kind == KIND_PAIRS) return (uint32_t)GBS_PAIRS_MID_BLOCK * GBS_PAIRS_MID_ITEMS;
     if (kind != KIND_KEYS) return 1024u * (GBS_WIDE_ITEMS * 5 / 8);
     return B == 1 ? (uint32_t)GBS_MID_TOP_BLOCK * GBS_MID_TOP_ITEMS : 512u * GBS_MID_KEYS_ITEMS_NESTED;
 }
@@ -204,7 +223,7 @@ static uint32_t mid_cap(int kind, uint32_t B)
 #endif
 static void tier_cuts(int kind, const Node& nd, uint32_t tile, uint32_t cuts[3])
 {
-    cuts[0] = tile / 2;
+    cuts[0] = kind == KIND_PAIRS ? (uint32_t)GBS_PAIRS_T0_BLOCK * GBS_PAIRS_T0_ITEMS : tile / 2;
     cuts[1] = GBS_MID_STEP9 ? mid_cap(kind, nd.B) : tile;
     cuts[2] = cuts[1];
     if (GBS_MID_STEP9 && kind == KIND_KEYS && nd.B == 1 && GBS_MID2_TOP_ITEMS > 0)
@@ -563,7 +582,7 @@ static void launch_seg(const LevelDev& lv, bool small, unsigned grid, cudaStream
 {
     if (small) launch_seg_t<KIND, GBS_SMALL, MODE>(lv, grid, st);
     else if constexpr (KIND == KIND_KEYS) launch_seg_t<KIND, GBS_BIG_KEYS, MODE>(lv, grid, st);
-    else launch_seg_t<KIND, GBS_BIG_WIDE, MODE>(lv, grid, st);
+    else launch_seg_t<KIND, BIGB(KIND), BIGI(KIND), MODE>(lv, grid, st);
 }
 
 template <int KIND>
@@ -803,10 +822,10 @@ static gbs_status_t launch_step9(const LevelDev& lv, const Node& nd, char* ws, c
                 if (nd.hi > cuts[2]) {   // the full tile
                     if constexpr (MODE == MODE_BUCKET && GBS_RARE_PERSIST) {
                         if constexpr (KIND == KIND_KEYS) launch_rare_t<KIND, GBS_BIG_KEYS>(tl[3], count, s23);
-                        else launch_rare_t<KIND, GBS_BIG_WIDE>(tl[3], count, s23);
+                        else launch_rare_t<KIND, BIGB(KIND), BIGI(KIND)>(tl[3], count, s23);
                     } else {
                         if constexpr (KIND == KIND_KEYS) launch_seg_t<KIND, GBS_BIG_KEYS, MODE>(tl[3], count, s23);
-                        else launch_seg_t<KIND, GBS_BIG_WIDE, MODE>(tl[3], count, s23);
+                        else launch_seg_t<KIND, BIGB(KIND), BIGI(KIND), MODE>(tl[3], count, s23);
                     }
                     GBS_LAUNCHED();
                 }
@@ -826,11 +845,14 @@ static gbs_status_t launch_step9(const LevelDev& lv, const Node& nd, char* ws, c
                 GBS_LAUNCHED();
             } else {   // no mid tier: (C/2, C] on the full tile
                 if constexpr (KIND == KIND_KEYS) launch_seg_t<KIND, GBS_BIG_KEYS, MODE>(tl[1], count, s12);
-                else launch_seg_t<KIND, GBS_BIG_WIDE, MODE>(tl[1], count, s12);
+                else launch_seg_t<KIND, BIGB(KIND), BIGI(KIND), MODE>(tl[1], count, s12);
                 GBS_LAUNCHED();
             }
             // (pairs on 256 x 32 instead: C4 78.8 -> 81.7 ms)
-            launch_seg_t<KIND, 512, ITEMS, MODE>(tl[0], count, st);
+            if constexpr (KIND == KIND_PAIRS)
+                launch_seg_t<KIND, GBS_PAIRS_T0_BLOCK, GBS_PAIRS_T0_ITEMS, MODE>(tl[0], count, st);
+            else
+                launch_seg_t<KIND, 512, ITEMS, MODE>(tl[0], count, st);
             GBS_LAUNCHED();
             if (ss) {
                 GBS_CUDA(cudaEventRecord(join, ss));

@@ -358,6 +358,8 @@ struct Seg {
 //     after the first round pair with no swap (one round pair when the keys never
 //     collide in their prefix: a key range below 2^(32-POSB), equal keys, presorted runs).
 // Uniform keys over a tile of 2^14 give groups of 1-4 items (2-3 round pairs).  A tile
+// whose key range fits the prefix (shift 0: the prefix is key - min itself) needs neither
+// the gather nor the fix-up, and its keys are read back from P (MODE_EXACT).  A tile
 // whose groups need more than PK_MAX_ITERS round pairs (a long unsorted run of keys
 // sharing a prefix) is sorted as (key << 32 | position) composites instead, in the same
 // shared memory: the result is identical either way (the stable sort), only the cost
@@ -380,8 +382,13 @@ struct Seg<KIND_PAIRS, BLOCK, ITEMS> {
     struct Ctrl {
         uint32_t mn[NW], mx[NW];          // key range reduction
         uint32_t fP[NW], fK[NW], lP[NW], lK[NW];   // first / last item of every warp
-        int fb;                           // 1: the tile was sorted as composites
+        int mode;                         // MODE_FIXED, MODE_EXACT or MODE_COMPOSITE
+        uint32_t klo;                     // MODE_EXACT: key = klo + (P >> POSB)
     };
+    // MODE_EXACT: the key range fits the prefix (shift 0), so the prefix is key - min
+    // itself and the packed sort alone is the stable order (no gather, no fix-up);
+    // MODE_FIXED: sorted keys in ksm after the fix-up; MODE_COMPOSITE: the fallback
+    enum { MODE_FIXED = 0, MODE_EXACT = 1, MODE_COMPOSITE = 2 };
     // shared memory: [ psm u32 | ksm u32 ] (or the fallback's u64 array) | vsm u32 | Ctrl
     __host__ __device__ static constexpr size_t region_bytes() { return 8 * (size_t)CS::SMEM_ELEMS; }
     __host__ __device__ static constexpr size_t smem_bytes()
@@ -495,7 +502,7 @@ struct Seg<KIND_PAIRS, BLOCK, ITEMS> {
         Ctrl* c = ctrl_of(smem);
         const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
         const int p0 = CS::load_pos(0);
-        // keys parked at their positions; the tile's key range
+        // keys parked at their positions (the fix-up gathers them); the tile's key range
         uint32_t lo = 0xFFFFFFFFu, hi = 0;
 #pragma unroll
         for (int k = 0; k < ITEMS; ++k) {
@@ -527,7 +534,12 @@ struct Seg<KIND_PAIRS, BLOCK, ITEMS> {
             const int p = p0 + 32 * k;
             x[k] = p < v ? (((x[k] - lo) >> shift) << POSB) | (uint32_t)p : 0xFFFFFFFFu;
         }
+        if (threadIdx.x == 0) {   // read by key_at / store after the sort's barriers
+            c->mode = shift ? MODE_FIXED : MODE_EXACT;
+            c->klo = lo;
+        }
         CS::sort(x, psm, v);     // x: the thread's sorted outputs [start, start + ITEMS)
+        if (shift == 0) return;  // (the sort ends on a barrier)
 
         // exact order inside prefix groups: odd-even transposition on (prefix, key)
         const int start = threadIdx.x * ITEMS;
@@ -583,7 +595,6 @@ struct Seg<KIND_PAIRS, BLOCK, ITEMS> {
                 break;
             }
         }
-        if (threadIdx.x == 0) c->fb = fb;
         if (!fb) {
             // every gather is done (the loop ends on a barrier): sorted keys and P in place
 #pragma unroll
@@ -594,7 +605,17 @@ struct Seg<KIND_PAIRS, BLOCK, ITEMS> {
             __syncthreads();
             return;
         }
-        // fallback: the stable sort of (key << 32 | position) composites
+        composite_sort(smem, v);
+    }
+
+    // fallback (cold, out of line so that its 64-bit registers do not weigh on the packed
+    // path): the stable sort of (key << 32 | position) composites of the parked keys
+    static __device__ __noinline__ void composite_sort(unsigned char* smem, int v)
+    {
+        Ctrl* c = ctrl_of(smem);
+        const uint32_t* ksm = ksm_of(smem);
+        const int p0 = CS::load_pos(0);
+        if (threadIdx.x == 0) c->mode = MODE_COMPOSITE;
         unsigned long long xx[ITEMS];
 #pragma unroll
         for (int k = 0; k < ITEMS; ++k) {
@@ -608,7 +629,10 @@ struct Seg<KIND_PAIRS, BLOCK, ITEMS> {
     // key of sorted item r (after sort)
     static __device__ __forceinline__ uint32_t key_at(unsigned char* smem, int r)
     {
-        if (ctrl_of(smem)->fb) return (uint32_t)(reinterpret_cast<const unsigned long long*>(smem)[CS::phys(r)] >> 32);
+        const Ctrl* c = ctrl_of(smem);
+        if (c->mode == MODE_EXACT) return c->klo + (psm_of(smem)[CS::phys(r)] >> POSB);
+        if (c->mode == MODE_COMPOSITE)
+            return (uint32_t)(reinterpret_cast<const unsigned long long*>(smem)[CS::phys(r)] >> 32);
         return ksm_of(smem)[CS::phys(r)];
     }
     static __device__ __forceinline__ uint32_t item_at(unsigned char* smem, int r) { return key_at(smem, r); }
@@ -619,7 +643,18 @@ struct Seg<KIND_PAIRS, BLOCK, ITEMS> {
         const uint32_t* vsm = vsm_of(smem);
         uint32_t* d = reinterpret_cast<uint32_t*>(dst) + dst_off;
         uint32_t* dv = dst_v + dst_off;
-        if (ctrl_of(smem)->fb) {
+        const Ctrl* c = ctrl_of(smem);
+        const uint32_t* psm = psm_of(smem);
+        if (c->mode == MODE_EXACT) {
+            const uint32_t klo = c->klo;
+            for (int p = threadIdx.x; p < v; p += BLOCK) {
+                const uint32_t P = psm[CS::phys(p)];
+                d[p] = xf_out(klo + (P >> POSB), xf);
+                dv[p] = vsm[P & PMASK];
+            }
+            return;
+        }
+        if (c->mode == MODE_COMPOSITE) {
             const unsigned long long* sm = reinterpret_cast<const unsigned long long*>(smem);
             for (int p = threadIdx.x; p < v; p += BLOCK) {
                 const unsigned long long cc = sm[CS::phys(p)];
@@ -628,7 +663,6 @@ struct Seg<KIND_PAIRS, BLOCK, ITEMS> {
             }
             return;
         }
-        const uint32_t* psm = psm_of(smem);
         const uint32_t* ksm = ksm_of(smem);
         for (int p = threadIdx.x; p < v; p += BLOCK) {
             d[p] = xf_out(ksm[CS::phys(p)], xf);

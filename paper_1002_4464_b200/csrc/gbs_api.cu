@@ -589,16 +589,16 @@ template <int KIND>
 static void launch_index(const LevelDev& lv, cudaStream_t st)
 {
     const size_t kb = key_bytes(KIND);
-    // streaming TMA form when every chunk start is 16-byte aligned (contiguous problems)
-    const bool tma = GBS_IDX_TMA && lv.pr.off == nullptr && ((uintptr_t)lv.srt & 15) == 0 &&
-                     (lv.pr.stride * kb) % 16 == 0 && ((size_t)lv.L * kb) % 16 == 0 && lv.s <= 8 * IDX_BLOCK;
+    // streaming TMA form (any item alignment: misaligned chunk starts are copied from the
+    // 16-byte boundary below)
+    const bool tma = GBS_IDX_TMA && (kb == 4 || kb == 8) && lv.s <= 8 * IDX_BLOCK;
     if (tma) {
-        const size_t sm = 2 * (size_t)IDX_CHUNK_BYTES + (size_t)lv.s * 12;
+        const size_t sm = 2 * ((size_t)IDX_CHUNK_BYTES + 16) + (size_t)lv.s * 12;
         static DevOnce once;
         const int occ = once.run([&] {
             set_smem(k_sample_index_tma<KIND, IDX_BLOCK, 8>, 220 * 1024);
             // occupancy at the largest table this kernel sees (s <= 4096)
-            return occupancy(k_sample_index_tma<KIND, IDX_BLOCK, 8>, IDX_BLOCK, 2 * (size_t)IDX_CHUNK_BYTES + 4096 * 12);
+            return occupancy(k_sample_index_tma<KIND, IDX_BLOCK, 8>, IDX_BLOCK, 2 * ((size_t)IDX_CHUNK_BYTES + 16) + 4096 * 12);
         });
         const unsigned grid = std::min<unsigned>(lv.B * lv.m, num_sms() * (unsigned)occ);
         launch_k(k_sample_index_tma<KIND, IDX_BLOCK, 8>, grid, IDX_BLOCK, sm, st, lv);

@@ -1149,18 +1149,22 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phas
 
 // Step 6, streaming form: persistent CTAs walk (sublist, 64 KB chunk) work items; one
 // thread keeps the next chunk's TMA bulk copy in flight (double buffer) while all
-// threads bisect the current one.  Used when every chunk start is 16-byte aligned
-// (contiguous problems; the host checks); per-splitter counts accumulate in registers.
+// threads bisect the current one; per-splitter counts accumulate in registers.  A bulk
+// copy needs 16-byte aligned addresses: a chunk that starts `lead` items past a 16-byte
+// boundary (nested problems start at bucket offsets) is copied from that boundary and
+// read at buffer + lead (the items copied before it are ignored; the last partial
+// 16 bytes are loaded by the threads).
 template <int KIND, int BLOCK, int MAXQ>
 __global__ void __launch_bounds__(BLOCK, (GBS_IDX_CHUNK_KB <= 32 ? 2 : 1)) k_sample_index_tma(LevelDev lv)
 {
     pdl_entry();
     using KT = typename std::conditional<KIND == KIND_U64, unsigned long long, uint32_t>::type;
     constexpr int CH = IDX_CHUNK_BYTES / sizeof(KT);
+    constexpr int LEAD = 16 / sizeof(KT);            // room for a misaligned chunk start
     extern __shared__ __align__(16) unsigned char smem_raw[];
     KT* buf0 = reinterpret_cast<KT*>(smem_raw);
-    KT* buf1 = buf0 + CH;
-    unsigned long long* gs = reinterpret_cast<unsigned long long*>(buf1 + CH);
+    KT* buf1 = buf0 + CH + LEAD;
+    unsigned long long* gs = reinterpret_cast<unsigned long long*>(buf1 + CH + LEAD);
     uint32_t* Q = reinterpret_cast<uint32_t*>(gs + lv.s);
     __shared__ __align__(8) unsigned long long bars[2];
 
@@ -1172,15 +1176,21 @@ __global__ void __launch_bounds__(BLOCK, (GBS_IDX_CHUNK_KB <= 32 ? 2 : 1)) k_sam
         const uint64_t i0 = (uint64_t)i * lv.L;
         return len > i0 ? (int)umin64(len - i0, lv.L) : 0;
     };
+    // first item of work item (tile t, chunk c) in HBM
+    auto chunk_src = [&](uint32_t t, int c) -> const KT* {
+        return reinterpret_cast<const KT*>(lv.srt) + lv.pr.offset(t / lv.m) + (uint64_t)(t % lv.m) * lv.L +
+               (uint64_t)c * CH;
+    };
+    auto lead_of = [&](const KT* src) -> int { return (int)(((uintptr_t)src & 15) / sizeof(KT)); };
     auto issue = [&](uint32_t t, int c, int slot) {   // thread 0 only
         const int v = tile_v(t);
         const int cl = min(CH, v - c * CH);
-        const unsigned bytes = (unsigned)((size_t)cl * sizeof(KT)) & ~15u;
-        const KT* src = reinterpret_cast<const KT*>(lv.srt) + lv.pr.offset(t / lv.m) + (uint64_t)(t % lv.m) * lv.L +
-                        (uint64_t)c * CH;
+        const KT* src = chunk_src(t, c);
+        const int ld = lead_of(src);
+        const unsigned bytes = (unsigned)((size_t)(ld + cl) * sizeof(KT)) & ~15u;
         unsigned long long* bar = &bars[slot];
         mbar_expect_tx(bar, bytes);
-        if (bytes) tma_load_1d(slot ? buf1 : buf0, src, bytes, bar);
+        if (bytes) tma_load_1d(slot ? buf1 : buf0, src - ld, bytes, bar);
     };
     if (threadIdx.x == 0) {
         mbar_init(&bars[0], 1);
@@ -1229,15 +1239,16 @@ __global__ void __launch_bounds__(BLOCK, (GBS_IDX_CHUNK_KB <= 32 ? 2 : 1)) k_sam
             }
             loaded_b = b;
         }
-        KT* ks = slot ? buf1 : buf0;
+        const KT* csrc = chunk_src(tile, chunk);
+        const int ld = lead_of(csrc);
+        KT* ks = (slot ? buf1 : buf0) + ld;
         mbar_wait(&bars[slot], (phase >> slot) & 1u);
         phase ^= 1u << slot;
         const int c0 = chunk * CH;
         const int cl = min(CH, v - c0);
         {   // keys past the last 16-byte boundary of the chunk (tail of the sublist)
-            const int full = (int)(((unsigned)((size_t)cl * sizeof(KT)) & ~15u) / sizeof(KT));
-            const KT* src = reinterpret_cast<const KT*>(lv.srt) + lv.pr.offset(b) + i0 + c0;
-            for (int p = full + threadIdx.x; p < cl; p += BLOCK) ks[p] = src[p];
+            const int full = (int)(((unsigned)((size_t)(ld + cl) * sizeof(KT)) & ~15u) / sizeof(KT)) - ld;
+            for (int p = max(full, 0) + threadIdx.x; p < cl; p += BLOCK) ks[p] = csrc[p];
         }
         __syncthreads();
         auto rank_key = [&](int p) -> unsigned long long {

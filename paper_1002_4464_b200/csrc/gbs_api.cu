@@ -712,6 +712,10 @@ struct HostPipe {
 #endif
 constexpr uint32_t HP_CHUNK_TILES = 64;   // sublists per H2D chunk (8 MB of keys)
 constexpr uint32_t HP_GROUPS = 16;        // Step 9 bucket groups (D2H chunks)
+#ifndef GBS_HP_NEST_GROUPS
+#define GBS_HP_NEST_GROUPS 32  // groups of a nested Step 9's problems (D2H chunks): C4 e2e 8 -> 32: 337 -> 326 ms
+#endif
+constexpr uint32_t HP_NEST_GROUPS = GBS_HP_NEST_GROUPS;
 
 struct Bufs {
     void *in, *reloc, *out;
@@ -725,17 +729,26 @@ struct Bufs {
     const uint32_t* scnt = nullptr;
 };
 
+// A window of a node's problems: [b0, b0 + bn) (bn = 0: all B).  Bufs / Probs passed to
+// exec describe all B problems; exec_kind offsets them and the node's own per-problem
+// workspace arrays by b0, and a nested child's window is [b0 s, (b0 + bn) s).  Used by
+// the host-pipelined call to finish a nested level in groups of problems, so that the
+// D2H copy of each group's final output overlaps the next groups' sorts.
+struct Win {
+    uint32_t b0 = 0, bn = 0;
+};
+
 template <int KIND>
 static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, Probs pr, cudaStream_t st, int stop,
-                              const HostPipe* hp);
+                              const HostPipe* hp, Win win);
 
 static gbs_status_t exec(const Plan& P, int ni, char* ws, const Bufs& bf, Probs pr, cudaStream_t st, int stop,
-                         const HostPipe* hp = nullptr)
+                         const HostPipe* hp = nullptr, Win win = Win())
 {
     switch (P.nodes[ni].kind) {
-        case KIND_KEYS: return exec_kind<KIND_KEYS>(P, ni, ws, bf, pr, st, stop, hp);
-        case KIND_PAIRS: return exec_kind<KIND_PAIRS>(P, ni, ws, bf, pr, st, stop, hp);
-        default: return exec_kind<KIND_U64>(P, ni, ws, bf, pr, st, stop, hp);
+        case KIND_KEYS: return exec_kind<KIND_KEYS>(P, ni, ws, bf, pr, st, stop, hp, win);
+        case KIND_PAIRS: return exec_kind<KIND_PAIRS>(P, ni, ws, bf, pr, st, stop, hp, win);
+        default: return exec_kind<KIND_U64>(P, ni, ws, bf, pr, st, stop, hp, win);
     }
 }
 
@@ -791,7 +804,7 @@ static gbs_status_t launch_step9(const LevelDev& lv, const Node& nd, char* ws, c
             // 5/8-tile configuration (keys: 512 threads, still 2 CTAs per SM); the rare
             // larger ones on the full tile.  Each tier launches over its list (built by
             // k_bucket_tiers).
-            const uint32_t count = nd.B * nd.s;
+            const uint32_t count = lv.B * nd.s;
             uint32_t* lists = reinterpret_cast<uint32_t*>(ws + nd.o_tiers);
             uint32_t* lens = lists + 4 * (uint64_t)count;
             uint32_t cuts[3];
@@ -861,7 +874,7 @@ static gbs_status_t launch_step9(const LevelDev& lv, const Node& nd, char* ws, c
                 GBS_CUDA(cudaStreamWaitEvent(st, join2, 0));
             }
         } else {
-            launch_seg<KIND, MODE>(lv, nd.bucket_small, nd.B * nd.s, st);
+            launch_seg<KIND, MODE>(lv, nd.bucket_small, lv.B * nd.s, st);
         }
         GBS_LAUNCHED();
     }
@@ -876,7 +889,7 @@ static gbs_status_t launch_step9(const LevelDev& lv, const Node& nd, char* ws, c
 static gbs_status_t launch_step9_pair(const LevelDev& lv, const Node& nd, char* ws, cudaStream_t st)
 {
     constexpr int KIND = KIND_KEYS;
-    const uint32_t count = nd.B * nd.s;
+    const uint32_t count = lv.B * nd.s;
     uint32_t* lists = reinterpret_cast<uint32_t*>(ws + nd.o_tiers);
     uint32_t* lens = lists + 4 * (uint64_t)count;
     GBS_CUDA(cudaMemsetAsync(lens, 0, 16, st));
@@ -913,14 +926,35 @@ static gbs_status_t launch_step9_pair(const LevelDev& lv, const Node& nd, char* 
 }
 
 template <int KIND>
-static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, Probs pr, cudaStream_t st, int stop,
-                              const HostPipe* hp)
+static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf_all, Probs pr, cudaStream_t st,
+                              int stop, const HostPipe* hp, Win win)
 {
     const Node& nd = P.nodes[ni];
+    // the window: problems [b0, b0 + B) of the node (everything indexed by problem is
+    // offset by b0 below; kernels index problems relative to it)
+    const uint32_t b0 = win.b0, B = win.bn ? win.bn : nd.B;
+    Bufs bf = bf_all;
+    if (b0) {
+        if (pr.off) pr.off += b0;
+        if (pr.len) pr.len += b0;
+        if (!pr.off) {   // contiguous problems: the data pointers move
+            const size_t o = (size_t)b0 * pr.stride;
+            auto mv = [o](void* p, size_t eb) { return p ? (void*)((char*)p + o * eb) : p; };
+            const size_t kb = key_bytes(KIND);
+            bf.in = mv(bf.in, kb);
+            bf.reloc = mv(bf.reloc, kb);
+            bf.out = mv(bf.out, kb);
+            bf.srt = mv(bf.srt, kb);
+            bf.in_v = (uint32_t*)mv(bf.in_v, 4);
+            bf.reloc_v = (uint32_t*)mv(bf.reloc_v, 4);
+            bf.out_v = (uint32_t*)mv(bf.out_v, 4);
+        }
+        if (bf.scnt) bf.scnt += b0;
+    }
     LevelDev lv;
     memset(&lv, 0, sizeof lv);
     lv.pr = pr;
-    lv.B = nd.B;
+    lv.B = B;
     lv.N = (uint32_t)nd.N;
     lv.pad_base = nd.pad_base;
     lv.in = bf.in;
@@ -936,7 +970,7 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
     lv.seg_min = 0;
     lv.seg_max = 0xFFFFFFFFu;
     if (nd.leaf) {
-        launch_seg<KIND, MODE_LEAF>(lv, nd.small, nd.B, st);
+        launch_seg<KIND, MODE_LEAF>(lv, nd.small, B, st);
         GBS_LAUNCHED();
         return GBS_SUCCESS;
     }
@@ -944,18 +978,22 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
     lv.s = nd.s;
     lv.d = nd.d;
     lv.m = nd.m;
-    lv.samples = reinterpret_cast<u64*>(ws + nd.o_samples);
-    lv.splitters = reinterpret_cast<u64*>(ws + nd.o_splitters);
-    lv.a = reinterpret_cast<uint32_t*>(ws + nd.o_a);
-    lv.l = reinterpret_cast<uint32_t*>(ws + nd.o_l);
-    lv.state = reinterpret_cast<unsigned long long*>(ws + nd.o_state);
+    const uint64_t ms = (uint64_t)nd.m * nd.s, nblk = (nd.s + 31) / 32;
+    lv.samples = reinterpret_cast<u64*>(ws + nd.o_samples) + b0 * ms;
+    lv.splitters = reinterpret_cast<u64*>(ws + nd.o_splitters) + (uint64_t)b0 * nd.s;
+    lv.a = reinterpret_cast<uint32_t*>(ws + nd.o_a) + b0 * ms;
+    lv.l = reinterpret_cast<uint32_t*>(ws + nd.o_l) + b0 * ms;
+    lv.state = reinterpret_cast<unsigned long long*>(ws + nd.o_state) + b0 * nblk;
+    // the longest-run word (Step 7 -> Step 8) follows the look-back words of all B problems
+    uint32_t* maxrun = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned long long*>(ws + nd.o_state) + nd.B * nblk);
     // fused Step 8+9: Step 2 must not sort in place when the output is the input (the
     // bucket CTAs would overwrite runs other CTAs still gather), so it writes the sorted
     // sublists to the reloc buffer, which Step 8 no longer needs
     const bool fuse = nd.fuse89 && stop == 0 && !hp;
+    const HostPipe* hp9 = (hp && stop == 0) ? hp : nullptr;   // D2H under a nested Step 9 (top level)
     lv.srt = bf.srt ? bf.srt : lv.in;
     lv.srt_v = lv.in_v;
-    lv.pex = reinterpret_cast<uint32_t*>(ws + nd.o_pex);
+    lv.pex = reinterpret_cast<uint32_t*>(ws + nd.o_pex) + b0 * ms;
     if (fuse && lv.srt == lv.out) {
         lv.srt = lv.reloc;
         lv.srt_v = lv.reloc_v;
@@ -971,8 +1009,12 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
     }
     // zero Step 7's look-back words and its longest-run word before the level's first
     // kernel, where the memset delays nothing (between Steps 6 and 7 it would)
-    const unsigned nblk = (nd.s + 31) / 32;
-    GBS_CUDA(cudaMemsetAsync(lv.state, 0, (size_t)nd.B * nblk * 8 + 8, st));
+    if (B == nd.B) {   // the look-back words and the longest-run word are contiguous
+        GBS_CUDA(cudaMemsetAsync(lv.state, 0, (size_t)B * nblk * 8 + 8, st));
+    } else {
+        GBS_CUDA(cudaMemsetAsync(lv.state, 0, (size_t)B * nblk * 8, st));
+        GBS_CUDA(cudaMemsetAsync(maxrun, 0, 8, st));
+    }
     pm.mark();
 
     // Steps 2-3: local sort + local samples (one CTA per sublist)
@@ -1013,12 +1055,14 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
         if (r) return r;
     } else {
         const Node& c = P.nodes[nd.step4];
-        Bufs b4{lv.samples, c.leaf ? (void*)lv.samples : (void*)(ws + c.o_reloc), lv.samples, nullptr, nullptr, nullptr};
+        // (all B problems' arrays; the child applies this window to them)
+        u64* smp_all = reinterpret_cast<u64*>(ws + nd.o_samples);
+        Bufs b4{smp_all, c.leaf ? (void*)smp_all : (void*)(ws + c.o_reloc), smp_all, nullptr, nullptr, nullptr};
         // each sublist's s samples are sorted and contiguous: runs of length s
         // (a nested level sorts only the samples of each problem's non-empty sublists: the
         // rest are virtual sentinels already in their sorted places, k_child_desc)
-        Probs p4{nullptr, bf.scnt, (uint64_t)nd.m * nd.s, nd.m * nd.s, nd.s};
-        gbs_status_t r = exec(P, nd.step4, ws, b4, p4, st, 0);
+        Probs p4{nullptr, bf_all.scnt, (uint64_t)nd.m * nd.s, nd.m * nd.s, nd.s};
+        gbs_status_t r = exec(P, nd.step4, ws, b4, p4, st, 0, nullptr, Win{b0, B});
         if (r) return r;
     }
     if (stop == 4) return GBS_SUCCESS;
@@ -1027,7 +1071,7 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
     // Step 5 (global samples) is fused into Step 6's prologue; the stand-alone kernel
     // runs only when a caller stops right after Step 5 (stage parity).
     if (stop == 5) {
-        const uint64_t tot = (uint64_t)nd.B * nd.s;
+        const uint64_t tot = (uint64_t)B * nd.s;
         launch_k(k_global_samples, (unsigned)((tot + 255) / 256), 256, 0, st, lv);
         GBS_LAUNCHED();
         return GBS_SUCCESS;
@@ -1056,8 +1100,8 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
     pm.mark();
 
     // Step 7: column-major exclusive scan -> l
-    lv.maxrun = reinterpret_cast<uint32_t*>(lv.state + (size_t)nd.B * nblk);   // one word past the look-back words
-    launch_k(k_scan, nd.B * nblk, SCAN_BLOCK, 0, st, lv);
+    lv.maxrun = maxrun;
+    launch_k(k_scan, B * (unsigned)nblk, SCAN_BLOCK, 0, st, lv);
     GBS_LAUNCHED();
     if (stop == 7) return GBS_SUCCESS;
     pm.mark();
@@ -1120,20 +1164,55 @@ static gbs_status_t exec_kind(const Plan& P, int ni, char* ws, const Bufs& bf, P
             r9 = launch_step9<KIND, MODE_BUCKET>(lv, nd, ws, st);
         if (r9) return r9;
     } else {
-        lv.child_off = reinterpret_cast<u64*>(ws + nd.o_child_off);
-        lv.child_len = reinterpret_cast<uint32_t*>(ws + nd.o_child_len);
-        const uint64_t tot = (uint64_t)nd.B * nd.s;
+        // the nested problems of this window: [b0 s, (b0 + B) s)
+        u64* coff = reinterpret_cast<u64*>(ws + nd.o_child_off);
+        uint32_t* clen = reinterpret_cast<uint32_t*>(ws + nd.o_child_len);
+        lv.child_off = coff + (uint64_t)b0 * nd.s;
+        lv.child_len = clen + (uint64_t)b0 * nd.s;
+        const uint64_t tot = (uint64_t)B * nd.s;
         const Node& ch = P.nodes[nd.step9];
         uint32_t* scnt = (!ch.leaf && ch.step4 >= 0) ? reinterpret_cast<uint32_t*>(ws + nd.o_child_scnt) : nullptr;
-        launch_k(k_child_desc, (unsigned)((tot + 255) / 256), 256, 0, st, lv, scnt, ch.L, ch.s);
+        launch_k(k_child_desc, (unsigned)((tot + 255) / 256), 256, 0, st, lv, scnt ? scnt + (uint64_t)b0 * nd.s : nullptr,
+                 ch.L, ch.s);
         GBS_LAUNCHED();
         // the nested level sorts its problems in place in the reloc buffer and uses the
         // sublists' buffer (dead after Step 8) as its own relocation target
         Bufs b9{bf.reloc, bf.srt ? bf.srt : bf.in, bf.out, bf.reloc_v, bf.in_v, bf.out_v};
         b9.xf_out = bf.xf_out;   // the keys entered the sort at this level's Step 2
         b9.scnt = scnt;
-        Probs p9{lv.child_off, lv.child_len, 0, 0};
-        gbs_status_t r = exec(P, nd.step9, ws, b9, p9, st, 0);
+        Probs p9{coff, clen, 0, 0};
+        gbs_status_t r = GBS_SUCCESS;
+        if (hp9) {
+            // host-pipelined call: the nested level in groups of this level's buckets; once
+            // buckets [0, j1) are sorted, the output prefix [0, j1 m d - V) is final (R18),
+            // and its D2H copy overlaps the next groups
+            const uint64_t V = (uint64_t)nd.m * nd.L - hp9->n;
+            const uint32_t G = std::max(1u, nd.s / HP_NEST_GROUPS);
+            uint64_t done = 0;
+            cudaEvent_t ev = scratch_event(4);
+            if (!ev) return fail(GBS_ERROR_CUDA, "cannot create an event");
+            for (uint32_t j0 = 0; j0 < nd.s; j0 += G) {
+                const uint32_t j1 = std::min(nd.s, j0 + G);
+                r = exec(P, nd.step9, ws, b9, p9, st, 0, nullptr, Win{j0, j1 - j0});
+                if (r) return r;
+                const uint64_t lo_cnt = (uint64_t)j1 * nd.m * nd.d;
+                const uint64_t upto = j1 == nd.s ? hp9->n : std::min<uint64_t>(hp9->n, lo_cnt > V ? lo_cnt - V : 0);
+                if (upto > done) {
+                    GBS_CUDA(cudaEventRecord(ev, st));
+                    GBS_CUDA(cudaStreamWaitEvent(hp9->cout, ev, 0));
+                    GBS_CUDA(cudaMemcpyAsync(hp9->h + done, reinterpret_cast<uint32_t*>(bf.out) + done,
+                                             (upto - done) * 4, cudaMemcpyDeviceToHost, hp9->cout));
+                    if (hp9->hv)
+                        GBS_CUDA(cudaMemcpyAsync(hp9->hv + done, bf.out_v + done, (upto - done) * 4,
+                                                 cudaMemcpyDeviceToHost, hp9->cout));
+                    done = upto;
+                }
+            }
+            GBS_CUDA(cudaEventRecord(ev, hp9->cout));
+            GBS_CUDA(cudaStreamWaitEvent(st, ev, 0));      // the call completes on st
+        } else {
+            r = exec(P, nd.step9, ws, b9, p9, st, 0, nullptr, Win{b0 * nd.s, B * nd.s});
+        }
         if (r) return r;
     }
     pm.mark();
@@ -1500,7 +1579,8 @@ gbs_status_t gbs_sort_ex(uint32_t* d_keys, uint32_t* d_vals, size_t n, const gbs
 // End to end from pinned host buffers (keys, or keys + values).  Above HP_CHUNK_TILES
 // sublists the H2D copy is chunked so Step 2 sorts each chunk as it lands; with CTA
 // buckets (one level) the D2H copy of each bucket group's final output prefix (R18)
-// overlaps the remaining Step 9 groups; with a nested Step 9 the D2H copy follows it.
+// overlaps the remaining Step 9 groups; with a nested Step 9 the nested level runs in
+// groups of problems and each group's final output prefix is copied back under the next.
 static gbs_status_t run_sort_host(uint32_t* h_keys, uint32_t* h_vals, size_t n, uint32_t* d_keys, uint32_t* d_vals,
                                   void* d_ws, size_t ws_bytes, cudaStream_t st)
 {
@@ -1532,12 +1612,9 @@ static gbs_status_t run_sort_host(uint32_t* h_keys, uint32_t* h_vals, size_t n, 
                     pairs ? reinterpret_cast<uint32_t*>(w + top.o_reloc_v) : nullptr, d_vals};
             Probs pr{nullptr, nullptr, 0, (uint32_t)n};
             HostPipe hp{h_keys, h_vals, n, cin, cout};
+            // (a nested Step 9 copies each group of finished problems back itself)
             r = exec(P, 0, w, bf, pr, st, 0, &hp);
             if (r) return r;
-            if (top.step9 >= 0) {   // nested Step 9: the output is final when the level is
-                GBS_CUDA(cudaMemcpyAsync(h_keys, d_keys, bytes, cudaMemcpyDeviceToHost, st));
-                if (pairs) GBS_CUDA(cudaMemcpyAsync(h_vals, d_vals, bytes, cudaMemcpyDeviceToHost, st));
-            }
             return GBS_SUCCESS;
         }
     }

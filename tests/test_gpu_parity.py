@@ -313,6 +313,31 @@ def test_pair_buckets_vs_oracle(dev):
     assert np.array_equal(to_np(d), exp)
 
 
+@pytest.mark.parametrize("n,dist,pairs", [((1 << 25) + 7, "uniform", True), ((1 << 25) + 7, "det_duplicates", True),
+                                          ((1 << 25) + 7, "staggered", True), (1 << 28, "zero", False),
+                                          ((1 << 28) + 3, "uniform", False)])
+def test_host_e2e_nested(dev, n, dist, pairs):
+    """gbs_sort_{keys,pairs}_host with a nested plan: the nested level runs in groups of
+    the top level's buckets and each group's guaranteed-final output prefix (R18) is
+    copied back while the next groups sort.  Output = the plain (stable) sort."""
+    keys = gi.generate(dist, n, seed=6)
+    h = torch.from_numpy(keys.view(np.int32).copy()).pin_memory()
+    d = torch.empty(n, dtype=torch.int32, device=dev)
+    if pairs:
+        vals = gi.pair_values(n)
+        hv = torch.from_numpy(vals.view(np.int32).copy()).pin_memory()
+        dv = torch.empty(n, dtype=torch.int32, device=dev)
+        gbs.sort_pairs_host(h, hv, d, dv)
+        torch.cuda.synchronize()
+        order = np.argsort(keys, kind="stable")
+        assert np.array_equal(h.numpy().view(np.uint32), keys[order])
+        assert np.array_equal(hv.numpy().view(np.uint32), vals[order])
+    else:
+        gbs.sort_keys_host(h, d)
+        torch.cuda.synchronize()
+        assert np.array_equal(h.numpy().view(np.uint32), np.sort(keys))
+
+
 def test_pair_buckets_host_pipeline(dev):
     """gbs_sort_keys_host with the pair-bucket plan: chunked H2D + Step 2, bucket-group
     D2H of the final prefix while later CTA-pair groups sort."""

@@ -527,17 +527,19 @@ static void launch_seg_t(const LevelDev& lv, unsigned count, cudaStream_t st)
 #ifndef GBS_RARE_PERSIST
 #define GBS_RARE_PERSIST 1   // Step 9's full-tile tier on persistent CTAs (k_segment_sort_rare)
 #endif
-template <int KIND, int BLOCK, int ITEMS>
+template <int KIND, int BLOCK, int ITEMS, int MODE = MODE_BUCKET>
 static void launch_rare_t(const LevelDev& lv, unsigned count, cudaStream_t st)
 {
-    const size_t sm = Seg<KIND, BLOCK, ITEMS>::smem_bytes();
+    const size_t sm = MODE == MODE_GATHER
+                          ? gather_smem_offset<KIND, BLOCK, ITEMS>() + ((size_t)gather_max_m(KIND) + 1) * 8
+                          : Seg<KIND, BLOCK, ITEMS>::smem_bytes();
     static DevOnce once;
     const int occ = once.run([&] {
-        set_smem(k_segment_sort_rare<KIND, BLOCK, ITEMS>, sm);
-        return occupancy(k_segment_sort_rare<KIND, BLOCK, ITEMS>, BLOCK, sm);
+        set_smem(k_segment_sort_rare<KIND, BLOCK, ITEMS, MODE>, sm);
+        return occupancy(k_segment_sort_rare<KIND, BLOCK, ITEMS, MODE>, BLOCK, sm);
     });
-    launch_k(k_segment_sort_rare<KIND, BLOCK, ITEMS>, std::min<unsigned>(count, num_sms() * (unsigned)occ), BLOCK, sm,
-             st, lv);
+    launch_k(k_segment_sort_rare<KIND, BLOCK, ITEMS, MODE>, std::min<unsigned>(count, num_sms() * (unsigned)occ), BLOCK,
+             sm, st, lv);
 }
 
 // Step 2 on CTA pairs: persistent clusters of two (one CTA per SM)
@@ -833,9 +835,9 @@ static gbs_status_t launch_step9(const LevelDev& lv, const Node& nd, char* ws, c
             cudaStream_t s12 = ss ? ss : st, s23 = ss2 ? ss2 : st;
             if (GBS_MID_STEP9) {
                 if (nd.hi > cuts[2]) {   // the full tile
-                    if constexpr (MODE == MODE_BUCKET && GBS_RARE_PERSIST) {
-                        if constexpr (KIND == KIND_KEYS) launch_rare_t<KIND, GBS_BIG_KEYS>(tl[3], count, s23);
-                        else launch_rare_t<KIND, BIGB(KIND), BIGI(KIND)>(tl[3], count, s23);
+                    if constexpr (GBS_RARE_PERSIST) {
+                        if constexpr (KIND == KIND_KEYS) launch_rare_t<KIND, GBS_BIG_KEYS, MODE>(tl[3], count, s23);
+                        else launch_rare_t<KIND, BIGB(KIND), BIGI(KIND), MODE>(tl[3], count, s23);
                     } else {
                         if constexpr (KIND == KIND_KEYS) launch_seg_t<KIND, GBS_BIG_KEYS, MODE>(tl[3], count, s23);
                         else launch_seg_t<KIND, BIGB(KIND), BIGI(KIND), MODE>(tl[3], count, s23);
@@ -844,8 +846,9 @@ static gbs_status_t launch_step9(const LevelDev& lv, const Node& nd, char* ws, c
                 }
                 bool mid_done = false;
                 if constexpr (KIND == KIND_KEYS) {
-                    if (nd.B != 1) {
-                        launch_seg_t<KIND, 512, GBS_MID_KEYS_ITEMS_NESTED, MODE>(tl[1], count, s12);
+                    if (nd.B != 1) {   // nested: a sparse tier (see below)
+                        if (GBS_RARE_PERSIST) launch_rare_t<KIND, 512, GBS_MID_KEYS_ITEMS_NESTED, MODE>(tl[1], count, s12);
+                        else launch_seg_t<KIND, 512, GBS_MID_KEYS_ITEMS_NESTED, MODE>(tl[1], count, s12);
                         mid_done = true;
                     } else if (nd.hi > cuts[1] && cuts[2] > cuts[1]) {
                         // the second mid tier on persistent CTAs (usually few buckets)
@@ -854,7 +857,14 @@ static gbs_status_t launch_step9(const LevelDev& lv, const Node& nd, char* ws, c
                         GBS_LAUNCHED();
                     }
                 }
-                if (!mid_done) launch_seg_t<KIND, MID_BLOCK_OF(KIND), MID_ITEMS_OF(KIND), MODE>(tl[1], count, s12);
+                if (!mid_done) {
+                    // nested levels: buckets average a quarter of the bound, so the mid tier
+                    // is sparse -> persistent CTAs over its list
+                    if (nd.B != 1 && GBS_RARE_PERSIST)
+                        launch_rare_t<KIND, MID_BLOCK_OF(KIND), MID_ITEMS_OF(KIND), MODE>(tl[1], count, s12);
+                    else
+                        launch_seg_t<KIND, MID_BLOCK_OF(KIND), MID_ITEMS_OF(KIND), MODE>(tl[1], count, s12);
+                }
                 GBS_LAUNCHED();
             } else {   // no mid tier: (C/2, C] on the full tile
                 if constexpr (KIND == KIND_KEYS) launch_seg_t<KIND, GBS_BIG_KEYS, MODE>(tl[1], count, s12);

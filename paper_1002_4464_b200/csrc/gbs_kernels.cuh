@@ -1776,6 +1776,34 @@ __host__ __device__ constexpr size_t gather_smem_offset()
 // most sublists per problem the fused path stages (the plan falls back to Step 8 above)
 __host__ __device__ constexpr uint32_t gather_max_m(int kind) { return kind == KIND_KEYS ? 2048u : 1024u; }
 
+// Fused Step 8+9 for bucket idx: stage its run table (from l and P_i,j-1) in shared
+// memory behind the tile, gather, sort, store.  `bounded`: a launch over every bucket
+// that skips those outside [seg_min, seg_max).
+template <int KIND, int BLOCK, int ITEMS, typename A>
+__device__ __forceinline__ void sort_gathered(const LevelDev& lv, uint32_t idx, unsigned char* smem_raw, bool bounded)
+{
+    using KeyT = typename A::S::KeyT;
+    uint64_t off;
+    int v;
+    segment_of<MODE_BUCKET>(lv, idx, off, v);
+    if (v <= 0 || (bounded && ((uint32_t)v <= lv.seg_min || (uint32_t)v > lv.seg_max))) return;
+    // (an L2 prefetch of the next wave's runs measured no gain here)
+    const uint32_t b = idx / lv.s, j = idx % lv.s;
+    uint2* run = reinterpret_cast<uint2*>(smem_raw + gather_smem_offset<KIND, BLOCK, ITEMS>());
+    const uint64_t col0 = (uint64_t)b * lv.m * lv.s + j;          // (row 0, column j) of problem b
+    const uint32_t l0 = lv.l[col0];
+    for (uint32_t i = threadIdx.x; i < lv.m; i += BLOCK) {
+        const uint32_t lr = lv.l[col0 + (uint64_t)i * lv.s] - l0;
+        run[i] = make_uint2(lr, i * lv.L + lv.pex[col0 + (uint64_t)i * lv.s] - lr);
+    }
+    if (threadIdx.x == 0) run[lv.m] = make_uint2((uint32_t)v, 0u);
+    __syncthreads();
+    const uint64_t pb = lv.pr.offset(b);
+    GatherSrc g{reinterpret_cast<const KeyT*>(lv.srt) + pb, KIND == KIND_PAIRS ? lv.srt_v + pb : nullptr, run,
+                (int)lv.m};
+    A::run_gather(g, v, lv.out, lv.out_v, off, smem_raw, lv.xf_out);
+}
+
 // One CTA per segment (bucket or leaf problem), adaptive tile size.  The segment
 // pf_stride ahead (the next wave) is prefetched into L2.  (A persistent variant that
 // walked segments with a work counter and register prefetch measured ~8% slower: the
@@ -1794,25 +1822,7 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK <= 576 ? 2 : 1)) k_segment_sort(
             if (blockIdx.x >= *lv.tier_len) return;
             idx = lv.tier_list[blockIdx.x];
         }
-        uint64_t off;
-        int v;
-        segment_of<MODE_BUCKET>(lv, idx, off, v);
-        if (v <= 0 || (!lv.tier_list && ((uint32_t)v <= lv.seg_min || (uint32_t)v > lv.seg_max))) return;
-        // (an L2 prefetch of the next wave's runs measured no gain here)
-        const uint32_t b = idx / lv.s, j = idx % lv.s;
-        uint2* run = reinterpret_cast<uint2*>(smem_raw + gather_smem_offset<KIND, BLOCK, ITEMS>());
-        const uint64_t col0 = (uint64_t)b * lv.m * lv.s + j;          // (row 0, column j) of problem b
-        const uint32_t l0 = lv.l[col0];
-        for (uint32_t i = threadIdx.x; i < lv.m; i += BLOCK) {
-            const uint32_t lr = lv.l[col0 + (uint64_t)i * lv.s] - l0;
-            run[i] = make_uint2(lr, i * lv.L + lv.pex[col0 + (uint64_t)i * lv.s] - lr);
-        }
-        if (threadIdx.x == 0) run[lv.m] = make_uint2((uint32_t)v, 0u);
-        __syncthreads();
-        const uint64_t pb = lv.pr.offset(b);
-        GatherSrc g{reinterpret_cast<const KeyT*>(lv.srt) + pb, KIND == KIND_PAIRS ? lv.srt_v + pb : nullptr, run,
-                    (int)lv.m};
-        A::run_gather(g, v, lv.out, lv.out_v, off, smem_raw, lv.xf_out);
+        sort_gathered<KIND, BLOCK, ITEMS, A>(lv, idx, smem_raw, !lv.tier_list);
         return;
     }
     const void* src = MODE == MODE_LEAF ? lv.in : lv.reloc;
@@ -1854,23 +1864,28 @@ __global__ void __launch_bounds__(BLOCK, (BLOCK <= 576 ? 2 : 1)) k_segment_sort(
     A::run(src, src_v, off, v, lv.out, lv.out_v, smem_raw, MODE == MODE_LEAF ? lv.xf_in : 0, lv.xf_out);
 }
 
-// The full-tile size tier of Step 9 (buckets above 5/8 of a tile: rare, none for
-// uniform inputs) on persistent CTAs, one per SM, walking the tier's list: an empty
-// tier then costs one wave of CTAs that exit at once instead of one CTA per bucket slot
-// (whose 133 KB of shared memory each would block the concurrent small tier's CTAs).
-template <int KIND, int BLOCK, int ITEMS>
+// The sparse size tiers of Step 9 (the full tile; in nested levels, whose buckets
+// average a quarter of the bound, the mid tier too) on persistent CTAs walking the
+// tier's list: a sparse tier then costs one wave of CTAs instead of one CTA per bucket
+// slot (C4 level 2: 262,144 slots of a 165 KB CTA took 4.9 ms for an almost empty tier).
+// Relocated buckets (MODE_BUCKET) or gathered ones (MODE_GATHER, fused Step 8+9).
+template <int KIND, int BLOCK, int ITEMS, int MODE = MODE_BUCKET>
 __global__ void __launch_bounds__(BLOCK, (BLOCK <= 576 ? 2 : 1)) k_segment_sort_rare(LevelDev lv)
 {
     pdl_entry();
-    using A = Adapt<KIND, BLOCK, ITEMS, GBS_ADAPT_DEPTH>;
+    using A = Adapt<KIND, BLOCK, ITEMS, ((ITEMS & (ITEMS - 1)) == 0 || KIND == KIND_KEYS ? GBS_ADAPT_DEPTH : 0)>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const uint32_t len = *lv.tier_len;
     for (uint32_t q = blockIdx.x; q < len; q += gridDim.x) {
         if (q != blockIdx.x) __syncthreads();   // shared memory reused
-        uint64_t off;
-        int v;
-        segment_of<MODE_BUCKET>(lv, lv.tier_list[q], off, v);
-        A::run(lv.reloc, lv.reloc_v, off, v, lv.out, lv.out_v, smem_raw, 0, lv.xf_out);
+        if constexpr (MODE == MODE_GATHER) {
+            sort_gathered<KIND, BLOCK, ITEMS, A>(lv, lv.tier_list[q], smem_raw, false);
+        } else {
+            uint64_t off;
+            int v;
+            segment_of<MODE_BUCKET>(lv, lv.tier_list[q], off, v);
+            A::run(lv.reloc, lv.reloc_v, off, v, lv.out, lv.out_v, smem_raw, 0, lv.xf_out);
+        }
     }
 }
 

@@ -5,6 +5,8 @@
   Fig. 5 analogue: device time vs the sample count s at n = 2^25 and 2^26 with
       one-tile sublists (L = 2^15); small s gives buckets above one tile, i.e. a nested
       Step 9 (the plan reports it).
+  Pairs: the Fig. 3 analogue for stable (u32 key, u32 value) pairs, the headline's item
+      type (C4 = 2^30), checked against a stable library sort.
 
 Timing: input restored from a pristine copy outside the CUDA-event window, 3 warm-ups,
 median of `--reps` sorts.  Every sorted output is checked against torch.sort.
@@ -61,6 +63,34 @@ def time_sort(keys_np, cfg=None, reps=10, prof=False):
     return out
 
 
+def time_sort_pairs(keys_np, reps=10):
+    dev = torch.device("cuda:0")
+    n = keys_np.size
+    pristine = torch.from_numpy(keys_np.view(np.int32)).to(dev)
+    pv = torch.arange(n, dtype=torch.int32, device=dev)
+    d, dv = torch.empty_like(pristine), torch.empty_like(pv)
+    ws = gbs.Workspace(dev)
+    st = torch.cuda.current_stream()
+    times = []
+    for r in range(3 + reps):
+        d.copy_(pristine)
+        dv.copy_(pv)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        gbs.sort_pairs(d, dv, ws=ws)
+        e1.record(st)
+        torch.cuda.synchronize()
+        if r >= 3:
+            times.append(e0.elapsed_time(e1))
+    k64 = pristine.view(torch.uint32).to(torch.int64)
+    exp_k, exp_i = torch.sort(k64, stable=True)
+    ok = bool(torch.equal(d.view(torch.uint32).to(torch.int64), exp_k)) and bool(torch.equal(dv.to(torch.int64), exp_i))
+    del k64, exp_k, exp_i
+    ms = float(np.median(times))
+    return {"n": n, "ms": round(ms, 4), "ms_min": round(min(times), 4), "ms_max": round(max(times), 4),
+            "gpairs_per_s": round(n / ms / 1e6, 3), "sorted_ok": ok, "plan": gbs.plan(n, pairs=True)["levels"]}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=10)
@@ -72,6 +102,11 @@ def main():
         r = time_sort(gi.generate("uniform", n, seed=0), reps=args.reps)
         res["fig3_n_scaling"].append(r)
         print("n-scaling", r, flush=True)
+    res["pairs_n_scaling"] = []
+    for lg in (16, 20, 22, 24, 25, 26, 27, 28, 29, 30):
+        r = time_sort_pairs(gi.generate("uniform", 1 << lg, seed=0), reps=args.reps)
+        res["pairs_n_scaling"].append(r)
+        print("pairs n-scaling", r, flush=True)
     res["fig4_steps_c2"] = time_sort(gi.generate("uniform", 1 << 25, seed=0), reps=args.reps, prof=True)
     print("steps", res["fig4_steps_c2"], flush=True)
     for lg in (25, 26):
@@ -89,6 +124,10 @@ def main():
              "| n | ms | Gkeys/s | plan (L, s) per level | sorted |", "|---|---|---|---|---|"]
     for r in res["fig3_n_scaling"]:
         lines.append(f"| 2^{int(np.log2(r['n']))} | {r['ms']} | {r['gkeys_per_s']} | {r['plan']} | {r['sorted_ok']} |")
+    lines += ["", "## Pairs: Gpairs/s vs n (uniform u32 keys, values = index, stable)", "",
+              "| n | ms | Gpairs/s | plan (L, s) per level | sorted |", "|---|---|---|---|---|"]
+    for r in res["pairs_n_scaling"]:
+        lines.append(f"| 2^{int(np.log2(r['n']))} | {r['ms']} | {r['gpairs_per_s']} | {r['plan']} | {r['sorted_ok']} |")
     lines += ["", "## Fig. 4 analogue: per-step ms at n = 2^25", "",
               "| step | ms |", "|---|---|"]
     for k, v in res["fig4_steps_c2"]["steps_ms"].items():

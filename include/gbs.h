@@ -21,10 +21,15 @@
  *   - The result is bit-identical across runs and streams (deterministic: no
  *     atomics decide any output position).
  *   - Calls on distinct buffers/workspaces/streams may run concurrently.  Inside a call,
- *     Step 9's size tiers and the host-buffer copies run on side streams shared by all
- *     calls on a device (forked from and joined back into `stream` with events), so a
- *     call may be captured into a CUDA graph, but no other call on the same device may
- *     be enqueued while that capture is open.
+ *     Step 9's size tiers and the host-buffer copies run on side streams of the calling
+ *     thread (forked from and joined back into `stream` with events), so a call may be
+ *     captured into a CUDA graph; while that capture is open the same thread must not
+ *     enqueue another call on the same device.
+ *   - Latency-bound sizes (n <= 2^20, default plan): the first call with given (buffers,
+ *     n, workspace) runs directly and records its launch sequence into a cached CUDA
+ *     graph (32 kept, least recently used evicted); later calls with the same arguments
+ *     replay it on `stream`.  Not used while `stream` is being captured, while profiling
+ *     (gbs_profile_begin) or with GBS_DEBUG_SYNC.
  *   - Limits: n <= 2^31 items per call (32-bit tags, R10).
  */
 #ifndef GBS_H_

@@ -16,6 +16,7 @@
 #include <mutex>
 #include <type_traits>
 #include <vector>
+#include <vector>
 
 #include "../../include/gbs.h"
 #include "gbs_internal.h"
@@ -677,14 +678,15 @@ static uint32_t num_sms()
 // step (fork/join through events, so the call stays ordered on the caller's stream;
 // capturable into a CUDA graph).  Shared by concurrent calls: that only serialises the
 // side work, the dependencies stay per call.
+// Side streams per calling thread and device (like the scratch events): calls from
+// different threads never share one, so a call being captured into a graph (the caller's
+// capture, or the library's own for latency-bound sizes) cannot pull another thread's
+// work into it.
 static cudaStream_t side_stream(int k = 0)   // k: 0 = Step 9 tiers, 1 = H2D, 2 = D2H, 3 = more Step 9 tiers
 {
-    static std::mutex mu;
-    static cudaStream_t ss[64][4] = {};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    std::lock_guard<std::mutex> g(mu);
-    if (dev < 0 || dev >= 64 || k < 0 || k > 3) return nullptr;
+    static thread_local cudaStream_t ss[MAX_DEVICES][4] = {};
+    const int dev = cur_device();
+    if (k < 0 || k > 3) return nullptr;
     if (!ss[dev][k] && cudaStreamCreateWithFlags(&ss[dev][k], cudaStreamNonBlocking) != cudaSuccess) ss[dev][k] = nullptr;
     return ss[dev][k];
 }
@@ -1243,6 +1245,63 @@ static gbs_status_t check_device()
     return ok ? GBS_SUCCESS : fail(GBS_ERROR_UNSUPPORTED, "device is not sm_100 (Blackwell B200)");
 }
 
+// Latency-bound sizes: a sort of at most GBS_GRAPH_MAX_N items is a short chain of small
+// kernels whose cost is mostly the host's launch path.  Its launch sequence is fixed by
+// (n, kind, buffers, workspace) (static plan, no host sync), so the first call with a
+// given key captures it into a CUDA graph (on a per-thread capture stream) and every call
+// replays that graph on the caller's stream: one launch instead of a dozen.  Calls on a
+// stream that is itself being captured, profiled calls and debug runs enqueue directly.
+#ifndef GBS_GRAPH_MAX_N
+#define GBS_GRAPH_MAX_N (1u << 20)
+#endif
+constexpr size_t GRAPH_CACHE = 32;   // instantiated graphs kept (least recently used evicted)
+struct GraphKey {
+    uintptr_t k, v, ws;
+    size_t n, ws_bytes;
+    int xf, dev;
+    bool operator==(const GraphKey& o) const
+    {
+        return k == o.k && v == o.v && ws == o.ws && n == o.n && ws_bytes == o.ws_bytes && xf == o.xf && dev == o.dev;
+    }
+};
+struct GraphEnt {
+    GraphKey key;
+    cudaGraphExec_t exec;
+    uint64_t used;
+};
+static std::mutex g_graph_mu;
+static std::vector<GraphEnt> g_graphs;
+static uint64_t g_graph_tick = 0;
+
+static cudaGraphExec_t graph_find(const GraphKey& key)
+{
+    std::lock_guard<std::mutex> g(g_graph_mu);
+    for (auto& e : g_graphs)
+        if (e.key == key) {
+            e.used = ++g_graph_tick;
+            return e.exec;
+        }
+    return nullptr;
+}
+static void graph_put(const GraphKey& key, cudaGraphExec_t exec)
+{
+    std::lock_guard<std::mutex> g(g_graph_mu);
+    if (g_graphs.size() >= GRAPH_CACHE) {
+        auto lru = std::min_element(g_graphs.begin(), g_graphs.end(),
+                                    [](const GraphEnt& a, const GraphEnt& b) { return a.used < b.used; });
+        cudaGraphExecDestroy(lru->exec);   // (a launch in flight keeps its resources)
+        g_graphs.erase(lru);
+    }
+    g_graphs.push_back(GraphEnt{key, exec, ++g_graph_tick});
+}
+static cudaStream_t capture_stream()
+{
+    static thread_local cudaStream_t cs[MAX_DEVICES] = {};
+    const int d = cur_device();
+    if (!cs[d] && cudaStreamCreateWithFlags(&cs[d], cudaStreamNonBlocking) != cudaSuccess) cs[d] = nullptr;
+    return cs[d];
+}
+
 static gbs_status_t run_sort(uint32_t* keys, uint32_t* vals, size_t n, const gbs_config_t* cfg, int stop,
                              void* ws, size_t ws_bytes, cudaStream_t st, int xf = 0)
 {
@@ -1269,6 +1328,31 @@ static gbs_status_t run_sort(uint32_t* keys, uint32_t* vals, size_t n, const gbs
             (top.leaf || !vals) ? vals : reinterpret_cast<uint32_t*>(w + top.o_reloc_v), vals};
     bf.xf_in = bf.xf_out = xf;
     Probs pr{nullptr, nullptr, 0, (uint32_t)n};
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (n <= GBS_GRAPH_MAX_N && !cfg && !stop && !g_prof && !debug_sync() &&
+        cudaStreamIsCapturing(st, &cap) == cudaSuccess && cap == cudaStreamCaptureStatusNone) {
+        const GraphKey key{(uintptr_t)keys, (uintptr_t)vals, (uintptr_t)ws, n, ws_bytes, xf, cur_device()};
+        cudaGraphExec_t ge = graph_find(key);
+        if (ge) {
+            GBS_CUDA(cudaGraphLaunch(ge, st));
+            return GBS_SUCCESS;
+        }
+        // first call with this key: run it directly (this also does every one-time setup:
+        // kernel attributes, side streams, events), then record the same sequence into a
+        // graph for the next calls (capturing executes nothing)
+        const gbs_status_t rd = exec(P, 0, w, bf, pr, st, 0);
+        if (rd) return rd;
+        cudaStream_t cs = capture_stream();
+        if (cs && cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+            const gbs_status_t rc = exec(P, 0, w, bf, pr, cs, 0);
+            cudaGraph_t g = nullptr;
+            const cudaError_t ec = cudaStreamEndCapture(cs, &g);
+            if (!rc && ec == cudaSuccess && g && cudaGraphInstantiate(&ge, g, 0) == cudaSuccess) graph_put(key, ge);
+            if (g) cudaGraphDestroy(g);
+        }
+        cudaGetLastError();   // a failed capture only means no graph: the sort itself is done
+        return GBS_SUCCESS;
+    }
     return exec(P, 0, w, bf, pr, st, stop);
 }
 

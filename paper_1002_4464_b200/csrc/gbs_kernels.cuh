@@ -547,10 +547,65 @@ struct Seg<KIND_PAIRS, BLOCK, ITEMS> {
         uint32_t eqm = 0;        // bit i: items i and i+1 share a prefix (invariant under swaps)
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) K[i] = start + i < v ? ksm[CS::phys(x[i] & PMASK)] : 0xFFFFFFFFu;
+#pragma unroll   // (sentinels past v never move: they take no part in any group)
+        for (int i = 0; i + 1 < ITEMS; ++i)
+            eqm |= (start + i + 1 < v && (x[i] >> POSB) == (x[i + 1] >> POSB) ? 1u : 0u) << i;
+        // Odd-even transposition sorts a group of g items in g rounds (any starting
+        // parity), and groups never change (the prefixes are invariant), so when every
+        // group is known to be short the rounds run a fixed count with no convergence
+        // vote: g_max = the largest group, from the runs of eqm and the groups crossing a
+        // thread boundary (tail of t + head of t + 1); a group that may span three threads
+        // (a thread whose items all share one prefix) takes the voting loop instead.
+        constexpr uint32_t FULL = (ITEMS >= 33) ? 0xFFFFFFFFu : ((1u << (ITEMS - 1)) - 1u);
+        const bool full = eqm == FULL;
+        int rounds = -1;   // -1: vote until a round pair swaps nothing
+        {
+            uint32_t m = eqm;
+            int rint = 0;
+            while (m) {
+                m &= m >> 1;
+                ++rint;
+            }
+            const int lead = full ? ITEMS - 1 : __ffs(~eqm) - 1;            // leading ones of eqm
+            const int tail = full ? ITEMS - 1 : (eqm & (1u << (ITEMS - 2))) ? (ITEMS - 1 - (32 - __clz(~eqm & FULL))) : 0;
+            const uint32_t info = (uint32_t)lead | (full ? 0x10000u : 0u);
+            uint32_t nP = __shfl_down_sync(0xffffffffu, x[0], 1), nI = __shfl_down_sync(0xffffffffu, info, 1);
+            if (lane == 0) {
+                c->fP[w] = x[0];
+                c->fK[w] = info;
+            }
+            __syncthreads();
+            const bool has_next = threadIdx.x + 1 < BLOCK;
+            if (lane == 31 && has_next) {
+                nP = c->fP[w + 1];
+                nI = c->fK[w + 1];
+            }
+            int g = rint + 1;
+            bool lng = false;
+            if (has_next && start + ITEMS < v && (x[ITEMS - 1] >> POSB) == (nP >> POSB)) {
+                g = max(g, tail + 1 + (int)(nI & 0xFFFFu) + 1);
+                lng = full || (nI >> 16);
+            }
 #pragma unroll
-        for (int i = 0; i + 1 < ITEMS; ++i) eqm |= ((x[i] >> POSB) == (x[i + 1] >> POSB) ? 1u : 0u) << i;
+            for (int o = 16; o > 0; o >>= 1) {
+                g = max(g, __shfl_xor_sync(0xffffffffu, g, o));
+                lng |= __shfl_xor_sync(0xffffffffu, lng ? 1 : 0, o) != 0;
+            }
+            if (lane == 0) {
+                c->mx[w] = (uint32_t)g;
+                c->mn[w] = lng ? 1u : 0u;
+            }
+            __syncthreads();
+            uint32_t gm = 0, lm = 0;
+#pragma unroll
+            for (int q = 0; q < NW; ++q) {
+                gm = max(gm, c->mx[q]);
+                lm |= c->mn[q];
+            }
+            if (!lm && gm <= 2 * GBS_PK_MAX_ITERS) rounds = gm <= 1 ? 0 : (int)gm;
+        }
         int iter = 0, fb = 0;
-        for (;;) {
+        for (; rounds != 0;) {
             bool sw = false;
             if (eqm) {
 #pragma unroll
@@ -588,6 +643,12 @@ struct Seg<KIND_PAIRS, BLOCK, ITEMS> {
                 x[0] = lP;
                 K[0] = lK;
                 sw = true;
+            }
+            if (rounds > 0) {    // a fixed number of round pairs
+                __syncthreads(); // (c->fP / lP reused by the next round pair)
+                rounds -= 2;
+                if (rounds < 0) rounds = 0;
+                continue;
             }
             if (!__syncthreads_or(sw)) break;
             if (++iter == GBS_PK_MAX_ITERS) {

@@ -3,7 +3,9 @@ fix-up (gbs_kernels.cuh, Seg<KIND_PAIRS>): inputs built to hit each of its paths
 with the oracle (stable pairs, R7) element by element.
 
 - full-range uniform keys: prefix groups of 1-4 items, a few transposition round pairs;
-- clusters of keys sharing a prefix, written in random order: many round pairs;
+- clusters of 2-300 keys sharing a prefix, written in random order: the fixed round count
+  (groups of at most 32, within one thread or across one thread boundary), the voting
+  loop (longer groups) and the composite fallback;
 - a tile whose keys span 0 .. 2^32-1 while almost all of them lie below 2^14: one prefix
   group of the whole tile, unsorted -> the composite fallback;
 - equal keys inside a prefix group (stability inside the fix-up)."""
@@ -51,7 +53,7 @@ def test_full_range_uniform(dev, n):
 
 
 @pytest.mark.parametrize("n", [16384, (1 << 20) + 5])
-@pytest.mark.parametrize("cluster", [8, 40, 300])
+@pytest.mark.parametrize("cluster", [2, 3, 8, 16, 31, 32, 33, 40, 64, 300])
 def test_prefix_clusters(dev, n, cluster):
     """Uniform keys plus, every 4096 positions, `cluster` keys from one window of 2^14
     values (they share a prefix at full range) in random order, some of them equal."""

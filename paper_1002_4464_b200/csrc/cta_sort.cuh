@@ -90,7 +90,7 @@ __device__ __forceinline__ void reg_sort(T (&x)[M])
 }
 
 #ifndef GBS_SHFL_LEVELS
-#define GBS_SHFL_LEVELS 3   // first merge levels on warp shuffles, 4-byte items (0 = all through smem)
+#define GBS_SHFL_LEVELS 4   // first merge levels on warp shuffles, 4-byte keys (0 = all through smem; 4 vs 3: C2 -0.4 %, C3 -0.3 %)
 #endif
 #ifndef GBS_SHFL_LEVELS_WIDE
 #define GBS_SHFL_LEVELS_WIDE 1   // the same for 8-byte items (u64 composites, pairs): 1 measured +0.9% at C4, 2 slower
@@ -100,7 +100,7 @@ __device__ __forceinline__ void reg_sort(T (&x)[M])
 // pair): a merge pointer that runs past the end of its run then walks down the other run
 // from its far end, so no end-of-run checks are needed (see merge_thread).
 
-template <typename T, int BLOCK, int ITEMS, int CHAINS_ = 0>
+template <typename T, int BLOCK, int ITEMS, int CHAINS_ = 0, int SHFL_ = -1>
 struct CtaSort {
     static constexpr int TILE = BLOCK * ITEMS;
     // A tile that is not a power of two (BLOCK not a power of two, e.g. 544 x 32) has a
@@ -118,8 +118,11 @@ struct CtaSort {
     static constexpr int CHAINS = CHAINS_ > 0 ? CHAINS_ : ((ITEMS * sizeof(T) <= 256) ? 2 : 1);
     static constexpr T TMAX = ~T(0);
     // merge levels done with warp shuffles (power-of-two ITEMS only)
+    // (SHFL_ >= 0: the instantiation's own count)
     static constexpr int SHFL_LEVELS =
-        ((ITEMS & (ITEMS - 1)) == 0 && ITEMS >= 2) ? (sizeof(T) == 4 ? GBS_SHFL_LEVELS : GBS_SHFL_LEVELS_WIDE) : 0;
+        ((ITEMS & (ITEMS - 1)) == 0 && ITEMS >= 2)
+            ? (SHFL_ >= 0 ? SHFL_ : (sizeof(T) == 4 ? GBS_SHFL_LEVELS : GBS_SHFL_LEVELS_WIDE))
+            : 0;
 
     static __device__ __forceinline__ int phys(int p) { return p + (p >> PAD); }
 

@@ -364,6 +364,12 @@ struct Seg {
 // sharing a prefix) is sorted as (key << 32 | position) composites instead, in the same
 // shared memory: the result is identical either way (the stable sort), only the cost
 // differs.  Values are parked at their positions and gathered at the write-back.
+#ifndef GBS_PAIRS_SHFL_LEVELS
+#define GBS_PAIRS_SHFL_LEVELS 4   // packed pairs tiles of 32 items per thread: 4 warp-shuffle merge levels (C4 -0.35 ms vs 3)
+#endif
+#ifndef GBS_PAIRS_SHFL_LEVELS_SMALL
+#define GBS_PAIRS_SHFL_LEVELS_SMALL 3   // ... of 16 or fewer (Step 9 tiers: 4 measured +0.06 ms)
+#endif
 #ifndef GBS_PK_MAX_ITERS
 #define GBS_PK_MAX_ITERS 16
 #endif
@@ -371,7 +377,8 @@ template <int BLOCK, int ITEMS>
 struct Seg<KIND_PAIRS, BLOCK, ITEMS> {
     using T = uint32_t;                                   // register items: keys, then P
     using KeyT = uint32_t;                                // in HBM
-    using CS = CtaSort<uint32_t, BLOCK, ITEMS, GBS_KEYS_CHAINS>;
+    using CS = CtaSort<uint32_t, BLOCK, ITEMS, GBS_KEYS_CHAINS,
+                       (ITEMS >= 32 ? GBS_PAIRS_SHFL_LEVELS : GBS_PAIRS_SHFL_LEVELS_SMALL)>;
     using CS64 = CtaSort<unsigned long long, BLOCK, ITEMS, GBS_WIDE_CHAINS>;   // fallback
     static constexpr int TILE = CS::TILE;
     static constexpr int NW = BLOCK / 32;

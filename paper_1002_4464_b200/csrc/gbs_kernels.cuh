@@ -365,7 +365,7 @@ struct Seg {
 // shared memory: the result is identical either way (the stable sort), only the cost
 // differs.  Values are parked at their positions and gathered at the write-back.
 #ifndef GBS_PAIRS_SHFL_LEVELS
-#define GBS_PAIRS_SHFL_LEVELS 4   // packed pairs tiles of 32 items per thread: 4 warp-shuffle merge levels (C4 -0.35 ms vs 3)
+#define GBS_PAIRS_SHFL_LEVELS 5   // packed pairs tiles of 32 items per thread: 5 warp-shuffle merge levels (C4 57.6 / 57.3 / 57.0 ms with 3 / 4 / 5)
 #endif
 #ifndef GBS_PAIRS_SHFL_LEVELS_SMALL
 #define GBS_PAIRS_SHFL_LEVELS_SMALL 3   // ... of 16 or fewer (Step 9 tiers: 4 measured +0.06 ms)
